@@ -1,0 +1,179 @@
+/*
+ * nw.h -- C ABI of the B200 nested-Winograd convolution library (libnw.so).
+ *
+ * Implements the nested Winograd convolution of Jiang, Chen & Tsui,
+ * arXiv 2102.13272 ("P:n" = line n of the paper text, PAPER.md), forward pass
+ * only, for sm_100a.  A K x K filter (K <= 9, or K <= 18 at stride 2) is split
+ * into 3-tap tiles; an outer F(m_o, r_o) Winograd kernel runs over the tile
+ * grid and an inner F(m_i, 3) kernel inside each tile (Eq. 2.4-2.6),
+ * so the convolution becomes
+ *     nested input transform -> per-transform-point channel contraction ->
+ *     nested output transform.
+ * Stride 2 uses the stride-Winograd polyphase split (Eq. 2.7);
+ * a stride-2 transposed convolution uses output phases (R11).
+ *
+ * Conventions (all calls):
+ *  - Tensors are dense, contiguous, NCHW, caller-owned device memory, 16-byte
+ *    aligned.  x [N][Cin][H][W], w [Cout][Cin][K][K] (transposed plans:
+ *    [Cin][Cout][K][K], PyTorch's conv_transpose2d layout), y [N][Cout][Ho][Wo].
+ *    Storage dtype is fp32 or bf16 (NW_ATTR_DTYPE); arithmetic is fp32 or the
+ *    split-bf16 tensor-core scheme selected by NW_ATTR_MATH.
+ *  - Cross-correlation, no filter flip, zero padding `pad` on every side
+ *    (Eq. 2.1 read as in DESIGN.md#R1).
+ *  - Every call returning nw_status_t never throws, never exits and never
+ *    synchronises the device except nw_plan_finalize (one table upload).
+ *    Kernel work is enqueued on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream); errors from launches are reported as NW_ERR_CUDA after
+ *    cudaGetLastError, asynchronous faults surface on the next sync.
+ *  - A plan is immutable after its first use (finalize) and may be shared by
+ *    several threads and streams; each concurrent call brings its own
+ *    workspace.
+ */
+#ifndef NW_H_
+#define NW_H_
+
+#include <stddef.h>
+
+#if defined(NW_BUILD) && defined(__GNUC__)
+#define NW_API __attribute__((visibility("default")))
+#else
+#define NW_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nw_plan_st *nw_plan_t;  /* opaque, owned by the library */
+typedef struct CUstream_st *nw_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  NW_OK = 0,
+  NW_ERR_INVALID = 1,     /* bad argument (null pointer, m outside [1,6], size mismatch) */
+  NW_ERR_UNSUPPORTED = 2, /* valid but not built: K > 9*stride, stride not in {1,2}, no kernel for (m_o, r_o, m_i) */
+  NW_ERR_NOMEM = 3,       /* host allocation failed */
+  NW_ERR_CUDA = 4,        /* a CUDA runtime / driver call or a kernel launch failed */
+  NW_ERR_WORKSPACE = 5,   /* ws_bytes smaller than nw_workspace_size() */
+  NW_ERR_STATE = 6        /* nw_plan_set after the plan was finalized */
+} nw_status_t;
+
+typedef enum {
+  NW_MATH_FP32_SIMT = 0, /* CUDA-core FP32 pipeline: the accuracy reference */
+  NW_MATH_BF16X3 = 1,    /* tcgen05 kind::f16, V=Vh+Vl, U=Uh+Ul, M = Vh.Uh + Vh.Ul + Vl.Uh (default) */
+  NW_MATH_BF16 = 2       /* tcgen05 kind::f16 on Vh, Uh only: speed ceiling, fails 5e-3 (R12) */
+} nw_math_t;
+
+typedef enum { NW_DTYPE_F32 = 0, NW_DTYPE_BF16 = 1 } nw_dtype_t;
+
+typedef enum {
+  NW_ATTR_MATH = 0,           /* nw_math_t, default NW_MATH_BF16X3 */
+  NW_ATTR_DTYPE = 1,          /* nw_dtype_t of x, w, y; default NW_DTYPE_F32 */
+  NW_ATTR_TRANSPOSED = 2,     /* 0/1: transposed convolution (stride 2 only); default 0 */
+  NW_ATTR_OUTPUT_PADDING = 3, /* transposed only; default 0 */
+  NW_ATTR_OUTER_TAPS = 4,     /* r_o: 3 = paper's fixed 3x3 tile grid (default); 0 = mixed ceil(K'/3) (R8) */
+  NW_ATTR_PAD = 5,            /* zero padding on every side; default K/2 */
+  NW_ATTR_PRELU = 6           /* 0/1: fuse y = y >= 0 ? y : slope[c]*y into the store (slopes via nw_plan_set_prelu) */
+} nw_attr_t;
+
+/* Integer tables exported for bit-exact comparison with the CPU oracle
+ * (DESIGN.md "Plan tables").  Rationals are (num, den) int64 pairs in lowest
+ * terms, den > 0, row-major. */
+typedef enum {
+  NW_TABLE_BT = 0,         /* B^T_hat  P_a x L        composite input transform (B_o^T (x) B_i^T).Gather */
+  NW_TABLE_G = 1,          /* G_hat    P_a x 3*r_o    composite filter transform G_o (x) G_i */
+  NW_TABLE_AT = 2,         /* A^T_hat  M_a x P_a      composite output transform A_o^T (x) A_i^T */
+  NW_TABLE_GATHER = 3,     /* l_o*l_i entries: reordered-column entry (j, s) -> slice input 3j + s */
+  NW_TABLE_SCATTER = 4,    /* n_phase x M_a x (position, keep): output placement + redundant-term discard */
+  NW_TABLE_ORIGINS = 5,    /* [advance, n_phase, shift_0 .. shift_{n_phase-1}]: slice origins per axis */
+  NW_TABLE_PHASE_TAPS = 6, /* [mode, n_phase, Kp, (offset, taps[Kp]) per phase]: stride / transposed phase split, Eq. 2.7 */
+  NW_TABLE_DIMS = 7        /* [K, stride, transposed, m_o, r_o, m_i, l_o, l_i, P_a, L, M_a, P, Cin, Cout, Cin_e, Cout_e, Kp, n_phase, advance] */
+} nw_table_t;
+
+typedef struct {
+  int K, stride, transposed, pad, output_padding;
+  int m_outer, r_outer, m_inner;
+  int points_axis;   /* P_a = l_o * l_i */
+  int points;        /* P = P_a^2 transform points per slice (625 for F(3,3)(x)F(3,3)) */
+  int window;        /* L = 3(l_o - 1) + l_i input window per slice axis (17) */
+  int tile_out;      /* advance: distinct outputs per tile axis (9) */
+  int n_phase;       /* coverage phases per axis (2 for m_i = 2, else 1) */
+  int Kp;            /* per-axis taps after the stride/transposed phase split */
+  int cin, cout;     /* layer channels */
+  int cin_e, cout_e; /* contraction K / N after phase folding (4*Cin stride 2; 4*Cout transposed) */
+  int cin_pad, cout_pad; /* cin_e / cout_e rounded up to the tensor-core granule (16) */
+  int math, dtype;
+  size_t filter_bytes; /* bytes of U for nw_transform_filter */
+} nw_plan_info_t;
+
+/* Create a plan for a K x K convolution with the given stride (1 or 2) using
+ * the nested F(m_outer, r_o) (x) F(m_inner, 3) algorithm.
+ * Errors: NW_ERR_INVALID if out is NULL, K < 1, Cin/Cout < 1, m outside [1,6];
+ * NW_ERR_UNSUPPORTED if stride not in {1,2} or the per-axis filter is longer
+ * than 3*r_o.  On success *out owns host memory until nw_plan_destroy. */
+NW_API nw_status_t nw_plan(int K, int stride, int m_outer, int m_inner, int Cin, int Cout, nw_plan_t *out);
+
+/* Set an attribute before first use (NW_ERR_STATE afterwards). */
+NW_API nw_status_t nw_plan_set(nw_plan_t plan, nw_attr_t attr, long long value);
+
+/* Per-output-channel PReLU slopes (device pointer, Cout floats, caller-owned,
+ * must outlive every call using the plan); used when NW_ATTR_PRELU = 1. */
+NW_API nw_status_t nw_plan_set_prelu(nw_plan_t plan, const float *slopes_dev);
+
+/* Validate the attribute set, build the transform tables and upload them to the
+ * current device (synchronous, once).  Called implicitly by the first GPU call;
+ * host-only queries (info, tables, sizes, counts) do not need a device. */
+NW_API nw_status_t nw_plan_finalize(nw_plan_t plan);
+
+NW_API nw_status_t nw_plan_destroy(nw_plan_t plan);
+
+/* Geometry of the plan (host only; works without a GPU). */
+NW_API nw_status_t nw_plan_info(nw_plan_t plan, nw_plan_info_t *info);
+
+/* Copy table `which` (nw_table_t) as int64 into dst[0..cap); *n receives the
+ * full length (call with cap = 0 to size).  NW_ERR_INVALID if cap < length. */
+NW_API nw_status_t nw_plan_tables(nw_plan_t plan, int which, long long *dst, size_t cap, size_t *n);
+
+/* Output spatial size for an H x W input (Eq. 2.1 / transposed definition). */
+NW_API nw_status_t nw_output_size(nw_plan_t plan, int H, int W, int *Ho, int *Wo);
+
+/* Bytes of device workspace nw_conv_forward / _ola / _direct need for a batch
+ * of N images of H x W (V and M transform-domain tensors, DESIGN.md layout). */
+NW_API nw_status_t nw_workspace_size(nw_plan_t plan, int N, int H, int W, size_t *bytes);
+NW_API nw_status_t nw_workspace_size_ola(nw_plan_t plan, int N, int H, int W, size_t *bytes);
+NW_API nw_status_t nw_workspace_size_direct(nw_plan_t plan, int N, int H, int W, size_t *bytes);
+
+/* Nested filter transform: phase split (stride / transposed),
+ * zero-pad to 3r_o x 3r_o taps, U = G_hat W G_hat^T, rounded once to the math
+ * mode's storage (fp32, or bf16 hi/lo planes).  w: device, layout above;
+ * U: device, info.filter_bytes, layout [P][cout_pad][cin_pad] (per plane). */
+NW_API nw_status_t nw_transform_filter(nw_plan_t plan, const void *w, void *U, nw_stream_t stream);
+
+/* Nested-Winograd forward: input transform -> contraction -> output
+ * transform (+ optional PReLU) into y.  x, U, y, ws device pointers;
+ * NW_ERR_WORKSPACE if ws_bytes < nw_workspace_size(plan, N, H, W). */
+NW_API nw_status_t nw_conv_forward(nw_plan_t plan, const void *x, const void *U, void *y,
+                            int N, int H, int W, void *ws, size_t ws_bytes, nw_stream_t stream);
+
+/* Comparison path: single-level OLA-Winograd F(3,3) (Eq. 2.3) with the
+ * ceil(K'/3)^2 block sum folded into the contraction; filter transformed from
+ * raw w inside the call (into ws). */
+NW_API nw_status_t nw_conv_ola(nw_plan_t plan, const void *x, const void *w, void *y,
+                        int N, int H, int W, void *ws, size_t ws_bytes, nw_stream_t stream);
+
+/* Comparison path: native convolution (Eq. 2.1) as an implicit GEMM. */
+NW_API nw_status_t nw_conv_direct(nw_plan_t plan, const void *x, const void *w, void *y,
+                           int N, int H, int W, void *ws, size_t ws_bytes, nw_stream_t stream);
+
+/* EWMM multiplications of one nested forward (slices * P * Cin_e * Cout_e). */
+NW_API nw_status_t nw_count_mults(nw_plan_t plan, int N, int H, int W, unsigned long long *ewmm);
+
+/* Number of kernels the library launched since load (host counter; for the
+ * bench's gpu_launches claim). */
+NW_API unsigned long long nw_launch_count(void);
+
+NW_API const char *nw_status_str(nw_status_t status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NW_H_ */

@@ -313,8 +313,10 @@ def layer_geometry(K: int, stride: int, transposed: bool, pad: int, output_paddi
     """
     if stride == 1:
         Kp = K
-    else:
+    elif not transposed:
         Kp = -(-K // 2)
+    else:
+        Kp = phase_taps(K, stride, True, pad)[2]
     r_o = outer_taps if outer_taps else max(1, -(-Kp // 3))
     cin_e = Cin * (4 if (stride == 2 and not transposed) else 1)
     cout_e = Cout * (4 if (stride == 2 and transposed) else 1)
@@ -374,8 +376,9 @@ def plan_tables(K: int, stride: int, m_o: int, m_i: int, Cin: int, Cout: int,
         kp = ax.keep(ph)
         for q in range(ax.M):
             scatter += [sh + pos[q], int(kp[q])]
+    taps = phase_taps(K, stride, transposed, pad)
     dims = [K, stride, int(transposed), m_o, r_o, m_i, ax.l_o, ax.l_i, ax.P, ax.L, ax.M,
-            ax.P * ax.P, Cin, Cout, cin_e, cout_e, Kp, len(ax.shifts), ax.adv]
+            ax.P * ax.P, Cin, Cout, cin_e, cout_e, taps[2], len(ax.shifts), ax.adv]
     return {
         TABLE_BT: _frac_pairs(BT),
         TABLE_G: _frac_pairs(G),
@@ -383,7 +386,7 @@ def plan_tables(K: int, stride: int, m_o: int, m_i: int, Cin: int, Cout: int,
         TABLE_GATHER: gather,
         TABLE_SCATTER: scatter,
         TABLE_ORIGINS: [ax.adv, len(ax.shifts)] + ax.shifts,
-        TABLE_PHASE_TAPS: phase_taps(K, stride, transposed, pad),
+        TABLE_PHASE_TAPS: taps,
         TABLE_DIMS: dims,
     }
 

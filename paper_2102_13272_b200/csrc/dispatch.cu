@@ -1,0 +1,29 @@
+// dispatch.cu -- route a plan's (m_o, r_o, m_i) to its compiled transform kernels.
+#include "nw_internal.h"
+
+namespace nw {
+
+template <int MO, int RO, int MI>
+nw_status_t input_impl(const nw_plan_st*, const Geometry&, const void*, void*, cudaStream_t);
+template <int MO, int RO, int MI>
+nw_status_t output_impl(const nw_plan_st*, const Geometry&, const float*, void*, cudaStream_t);
+
+#define NW_DISPATCH_AXIS(p, FN, ...)                                       \
+  do {                                                                     \
+    const int mo_ = (p)->m_o, ro_ = (p)->r_o, mi_ = (p)->m_i;              \
+    if (mo_ == 3 && ro_ == 3 && mi_ == 3) return FN<3, 3, 3>(__VA_ARGS__); \
+    if (mo_ == 2 && ro_ == 3 && mi_ == 2) return FN<2, 3, 2>(__VA_ARGS__); \
+    if (mo_ == 3 && ro_ == 2 && mi_ == 3) return FN<3, 2, 3>(__VA_ARGS__); \
+    if (mo_ == 2 && ro_ == 3 && mi_ == 3) return FN<2, 3, 3>(__VA_ARGS__); \
+    return NW_ERR_UNSUPPORTED;                                             \
+  } while (0)
+
+nw_status_t launch_input_transform(const nw_plan_st* p, const Geometry& g, const void* x, void* V, cudaStream_t s) {
+  NW_DISPATCH_AXIS(p, input_impl, p, g, x, V, s);
+}
+
+nw_status_t launch_output_transform(const nw_plan_st* p, const Geometry& g, const float* M, void* y, cudaStream_t s) {
+  NW_DISPATCH_AXIS(p, output_impl, p, g, M, y, s);
+}
+
+}  // namespace nw

@@ -1,0 +1,61 @@
+// gemm_simt.cu -- G3s FP32 CUDA-core contraction (the accuracy reference path)
+#include "nw_internal.h"
+
+namespace nw {
+
+// ---------------------------------------------------------------------------
+// G3s: FP32 SIMT contraction, batched over transform points
+// M[xi][t][co] = sum_k V[xi][t][k] * U[xi][co][k]
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict__ V, const float* __restrict__ U,
+                                                        float* __restrict__ M, long long T_pad, int K, int Nn) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int xi = blockIdx.z;
+  const long long t0 = (long long)blockIdx.x * 64;
+  const int n0 = blockIdx.y * 64;
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  const float* Vb = V + ((long long)xi * T_pad + t0) * K;
+  const float* Ub = U + ((long long)xi * Nn + n0) * K;
+  float acc[4][4] = {};
+  const int lr = tid / 4, lk = (tid % 4) * 4;
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    const float4 a = *reinterpret_cast<const float4*>(Vb + (long long)lr * K + k0 + lk);
+    float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (n0 + lr < Nn) bb = *reinterpret_cast<const float4*>(Ub + (long long)lr * K + k0 + lk);
+    As[lk + 0][lr] = a.x; As[lk + 1][lr] = a.y; As[lk + 2][lr] = a.z; As[lk + 3][lr] = a.w;
+    Bs[lk + 0][lr] = bb.x; Bs[lk + 1][lr] = bb.y; Bs[lk + 2][lr] = bb.z; Bs[lk + 3][lr] = bb.w;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      float ar[4], br[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ar[i] = As[k][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) br[j] = Bs[k][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const long long t = t0 + ty * 4 + i;
+    float* dst = M + ((long long)xi * T_pad + t) * Nn + n0 + tx * 4;
+    if (n0 + tx * 4 + 3 < Nn) {
+      *reinterpret_cast<float4*>(dst) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    }
+  }
+}
+
+nw_status_t launch_gemm_simt(const nw_plan_st* p, const Geometry& g, const float* V, const float* U, float* M,
+                             cudaStream_t s) {
+  (void)p;
+  dim3 grid((unsigned)(g.T_pad / 64), (unsigned)((g.cout_pad + 63) / 64), (unsigned)g.P);
+  gemm_simt_kernel<<<grid, 256, 0, s>>>(V, U, M, g.T_pad, g.cin_pad, g.cout_pad);
+  return check_launch();
+}
+
+}  // namespace nw

@@ -1,0 +1,82 @@
+// nw_internal.h -- plan structure and launcher declarations shared by the
+// library's translation units (not part of the public ABI; see include/nw.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/nw.h"
+#include "cooktoom.cuh"
+
+namespace nw {
+
+constexpr int kMaxTaps = 12;
+constexpr int kGranule = 16;  // tensor-core K / N granule (kind::f16 K = 16, N % 16 == 0 at M = 128)
+
+// Geometry of one layer, computed by the planner (host) and passed by value to
+// the kernels.
+struct Geometry {
+  // per spatial axis (square filters, same on both axes)
+  int mode;          // 0 stride 1, 1 stride-2 input phases (Eq. 2.7), 2 transposed output phases
+  int SR;            // input-phase stride factor (2 for mode 1, else 1)
+  int n_sp;          // stride / output phases per axis (2 for modes 1, 2)
+  int Kp;            // taps per phase after the split
+  int off[2];        // per phase: mode 0 -pad; mode 1 p - pad; mode 2 -offset (input index offset)
+  int taps[2][kMaxTaps];  // per phase tap -> original filter tap index, -1 = zero
+  int adv, nph, shift[3];
+  // layer
+  int N, Cin, Cout, H, W, Ho, Wo;
+  int Hq, Wq;        // extent of the stride-1 output grid covered by slices (per phase for mode 2)
+  int tiles_h, tiles_w;
+  long long T, T_pad;       // slices, padded to the GEMM M tile
+  int cin_e, cout_e, cin_pad, cout_pad;
+  int P, Pa;
+};
+
+}  // namespace nw
+
+struct nw_plan_st {
+  int K, stride, m_o, m_i, Cin, Cout;
+  int math = NW_MATH_BF16X3;
+  int dtype = NW_DTYPE_F32;
+  int transposed = 0, output_padding = 0, outer_taps = 3, pad = -1, prelu = 0;
+  const float *slopes = nullptr;
+  bool finalized = false;
+  // derived at finalize
+  int Kp = 0, r_o = 0, cin_e = 0, cout_e = 0, cin_pad = 0, cout_pad = 0;
+  nw::NestedAxis ax{};
+};
+
+namespace nw {
+
+extern std::atomic<unsigned long long> g_launches;
+
+nw_status_t finalize(nw_plan_st *p);
+Geometry make_geometry(const nw_plan_st *p, int N, int H, int W);
+size_t v_bytes(const nw_plan_st *p, const Geometry &g);
+size_t m_bytes(const nw_plan_st *p, const Geometry &g);
+size_t filter_bytes(const nw_plan_st *p);
+
+// launchers (nested_kernels.cu)
+nw_status_t launch_filter_transform(const nw_plan_st *p, const Geometry &g, const void *w, void *U,
+                                    cudaStream_t s);
+nw_status_t launch_input_transform(const nw_plan_st *p, const Geometry &g, const void *x, void *V,
+                                   cudaStream_t s);
+nw_status_t launch_output_transform(const nw_plan_st *p, const Geometry &g, const float *M, void *y,
+                                    cudaStream_t s);
+nw_status_t launch_gemm_simt(const nw_plan_st *p, const Geometry &g, const float *V, const float *U,
+                             float *M, cudaStream_t s);
+// tcgen05 contraction (tc_gemm.cu)
+nw_status_t launch_gemm_tc(const nw_plan_st *p, const Geometry &g, const void *V, const void *U,
+                           float *M, cudaStream_t s);
+
+inline nw_status_t check_launch() {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError() == cudaSuccess ? NW_OK : NW_ERR_CUDA;
+}
+
+inline long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
+
+}  // namespace nw

@@ -1,0 +1,93 @@
+"""C-ABI boundary on the CPU: the library loads, exports every declared symbol,
+validates arguments, and its planner tables equal the oracle's bit for bit."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from oracle import counts
+from oracle.nested import plan_tables
+from paper_2102_13272_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "nw.h")).read()
+    declared = set(re.findall(r"NW_API [\w\s\*]*?\b(nw_\w+)\(", hdr))
+    assert declared, "no declarations parsed"
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(_lib.EXPORTS)
+
+
+def test_status_strings_and_errors():
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    assert lib.nw_plan(9, 3, 3, 3, 4, 4, ctypes.byref(h)) == _lib.NW_ERR_UNSUPPORTED
+    assert lib.nw_plan(9, 1, 0, 3, 4, 4, ctypes.byref(h)) == _lib.NW_ERR_INVALID
+    assert lib.nw_plan(9, 1, 7, 3, 4, 4, ctypes.byref(h)) == _lib.NW_ERR_INVALID
+    assert lib.nw_plan(10, 1, 3, 3, 4, 4, ctypes.byref(h)) == _lib.NW_ERR_UNSUPPORTED
+    assert lib.nw_plan(9, 1, 3, 3, 4, 4, None) == _lib.NW_ERR_INVALID
+    assert lib.nw_plan(9, 1, 3, 3, 0, 4, ctypes.byref(h)) == _lib.NW_ERR_INVALID
+    assert _lib.status_str(_lib.NW_ERR_WORKSPACE) == "workspace too small"
+    p = _lib.Plan(5, 1, 3, 3, 4, 4)
+    with pytest.raises(_lib.NWError) as e:
+        lib2 = _lib.load()
+        st = lib2.nw_plan_set(p.handle, _lib.ATTR_MATH, 0)
+        _lib._chk(st, "late set")
+    assert e.value.status == _lib.NW_ERR_STATE
+    with pytest.raises(_lib.NWError):
+        _lib.Plan(5, 1, 3, 3, 4, 4, transposed=True)          # transposed needs stride 2
+
+
+CASES = [
+    # K, stride, m_o, m_i, Cin, Cout, transposed, pad, outer_taps
+    (5, 1, 2, 2, 16, 16, False, 2, 3),     # configs[0]
+    (5, 1, 3, 3, 64, 64, False, 2, 3),
+    (7, 1, 3, 3, 64, 64, False, 3, 3),
+    (9, 1, 3, 3, 64, 64, False, 4, 3),     # configs[1]
+    (9, 1, 3, 3, 256, 256, False, 4, 3),   # configs[2]
+    (7, 2, 3, 3, 3, 64, False, 3, 3),      # configs[3]
+    (9, 2, 3, 3, 64, 64, False, 4, 3),
+    (9, 2, 3, 3, 32, 1, True, 4, 3),       # configs[4] deconv
+    (3, 2, 3, 3, 4, 4, True, 1, 3),
+    (5, 1, 3, 3, 8, 8, False, 2, 0),       # mixed outer kernel F(3,2)
+    (4, 1, 2, 3, 8, 8, False, 1, 3),
+    (8, 1, 4, 3, 8, 8, False, 3, 3),
+    (6, 1, 6, 6, 8, 8, False, 3, 3),
+    (3, 1, 1, 1, 8, 8, False, 1, 3),
+]
+
+
+@pytest.mark.parametrize("K,stride,m_o,m_i,Cin,Cout,tr,pad,ot", CASES)
+def test_tables_bit_exact_vs_oracle(K, stride, m_o, m_i, Cin, Cout, tr, pad, ot):
+    plan = _lib.Plan(K, stride, m_o, m_i, Cin, Cout, transposed=tr, pad=pad, outer_taps=ot,
+                     output_padding=1 if tr else 0)
+    ref = plan_tables(K, stride, m_o, m_i, Cin, Cout, transposed=tr, pad=pad, outer_taps=ot)
+    for which in range(8):
+        assert plan.tables(which) == ref[which], f"table {which}"
+
+
+@pytest.mark.parametrize("K,stride,m_o,m_i,Cin,Cout,tr,pad,ot", CASES[:9])
+def test_count_mults_vs_closed_form(K, stride, m_o, m_i, Cin, Cout, tr, pad, ot):
+    plan = _lib.Plan(K, stride, m_o, m_i, Cin, Cout, transposed=tr, pad=pad, outer_taps=ot,
+                     output_padding=1 if tr else 0)
+    N, H, W = 2, 37, 29
+    Ho, Wo = plan.output_size(H, W)
+    inf = plan.info()
+    if tr:
+        Hq, Wq = (Ho + 1) // 2, (Wo + 1) // 2
+    else:
+        Hq, Wq = Ho, Wo
+    ref = counts.layer_ewmm_nested(N, Hq, Wq, inf["cin_e"], inf["cout_e"], m_o, inf["r_outer"], m_i)
+    assert plan.count_mults(N, H, W) == ref
+
+
+def test_output_sizes():
+    assert _lib.Plan(9, 2, 3, 3, 32, 1, transposed=True, pad=4, output_padding=1).output_size(540, 960) == (1080, 1920)
+    assert _lib.Plan(7, 2, 3, 3, 3, 64, pad=3).output_size(224, 224) == (112, 112)
+    assert _lib.Plan(9, 2, 3, 3, 64, 64, pad=4).output_size(112, 112) == (56, 56)
+    assert _lib.Plan(9, 1, 3, 3, 256, 256, pad=4).output_size(64, 64) == (64, 64)

@@ -1,0 +1,92 @@
+"""GPU parity of the nested-Winograd path (through the C ABI) against the FP64 oracle.
+
+Metric (BASELINE north_star, R14): max|y - y_ref| / max|y_ref| with
+y_ref = oracle.direct in float64 from the stored (cast) x and w.
+Tolerances: 1e-4 for the FP32 CUDA-core path, 5e-3 for the tensor-core path.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import direct
+from oracle.errstudy import rel_err
+from oracle.phases import conv_transpose2d_phases
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-4, "bf16x3": 5e-3}
+
+
+def _math(name):
+    from paper_2102_13272_b200 import MATH_BF16X3, MATH_FP32_SIMT
+    return {"fp32": MATH_FP32_SIMT, "bf16x3": MATH_BF16X3}[name]
+
+
+def _run(layer, math, prelu=False):
+    from paper_2102_13272_b200 import NestedConv2d
+    t = synth.make_inputs(layer)
+    x, w = t["x"].cuda(), t["w"].cuda()
+    slopes = None
+    if layer.prelu or prelu:
+        slopes = torch.full((layer.Cout,), synth.PRELU_SLOPE, device="cuda")
+    conv = NestedConv2d(w, layer.stride, layer.pad, layer.m_o, layer.m_i, _math(math),
+                        transposed=layer.transposed, output_padding=layer.output_padding,
+                        prelu_slopes=slopes)
+    y = conv(x)
+    torch.cuda.synchronize()
+    return t, y.float().cpu().numpy()
+
+
+def _ref(layer, t):
+    x = t["x"].double().numpy()
+    w = t["w"].double().numpy()
+    if layer.transposed:
+        y = direct.conv_transpose2d(x, w, layer.stride, layer.pad, layer.output_padding)
+    else:
+        y = direct.conv2d(x, w, layer.stride, layer.pad)
+    if layer.prelu:
+        y = np.where(y >= 0, y, synth.PRELU_SLOPE * y)
+    return y
+
+
+SMALL = {
+    "c1": synth.CONFIGS["c1"],
+    "c2k5": synth.small(synth.CONFIGS["c2k5"], N=2, H=40, W=31),
+    "c2k7": synth.small(synth.CONFIGS["c2k7"], N=2, H=40, W=31),
+    "c2k9": synth.small(synth.CONFIGS["c2k9"], N=2, H=40, W=31),
+    "c3": synth.small(synth.CONFIGS["c3"], N=1, H=29, W=36, Cin=64, Cout=48),
+    "c4a": synth.small(synth.CONFIGS["c4a"], N=2, H=45, W=38),
+    "c4b": synth.small(synth.CONFIGS["c4b"], N=1, H=40, W=36, Cin=32, Cout=32),
+    "c5_conv1": synth.small(synth.CONFIGS["c5_conv1"], N=1, H=30, W=41),
+    "c5_deconv": synth.small(synth.CONFIGS["c5_deconv"], N=1, H=19, W=23),
+}
+
+
+@pytest.mark.parametrize("name", list(SMALL))
+def test_fp32_simt_parity(name):
+    layer = SMALL[name]
+    t, y = _run(layer, "fp32")
+    ref = _ref(layer, t)
+    assert y.shape == ref.shape
+    tol = TOL["fp32"] if layer.dtype == "f32" else 2.0 ** -8  # bf16 output storage adds <= 2^-9 rel
+    err = rel_err(y, ref)
+    assert err <= tol, err
+
+
+def test_mixed_outer_kernel_fp32():
+    layer = synth.small(synth.CONFIGS["c2k5"], N=1, H=33, W=20, Cin=16, Cout=16)
+    from paper_2102_13272_b200 import NestedConv2d
+    t = synth.make_inputs(layer)
+    conv = NestedConv2d(t["w"].cuda(), 1, 2, 3, 3, _math("fp32"), outer_taps=0)
+    assert conv.info["r_outer"] == 2 and conv.info["points"] == 400
+    y = conv(t["x"].cuda()).cpu().numpy()
+    assert rel_err(y, _ref(layer, t)) <= TOL["fp32"]
+
+
+def test_deterministic_and_no_nan():
+    layer = SMALL["c2k9"]
+    _, y1 = _run(layer, "fp32")
+    _, y2 = _run(layer, "fp32")
+    assert np.array_equal(y1, y2)
+    assert np.isfinite(y1).all()
