@@ -164,6 +164,23 @@ NW_API nw_status_t nw_conv_ola(nw_plan_t plan, const void *x, const void *w, voi
 NW_API nw_status_t nw_conv_direct(nw_plan_t plan, const void *x, const void *w, void *y,
                            int N, int H, int W, void *ws, size_t ws_bytes, nw_stream_t stream);
 
+/* End-to-end form of nw_conv_forward on HOST buffers: x_host -> device copy
+ * (cudaMemcpyAsync into ws), the forward pass, y -> y_host, all enqueued on
+ * `stream`.  Pinned host memory makes the copies asynchronous.  ws must hold
+ * nw_workspace_size_host() bytes (forward workspace + device x and y). */
+NW_API nw_status_t nw_workspace_size_host(nw_plan_t plan, int N, int H, int W, size_t *bytes);
+NW_API nw_status_t nw_conv_forward_host(nw_plan_t plan, const void *x_host, const void *U, void *y_host,
+                                        int N, int H, int W, void *ws, size_t ws_bytes, nw_stream_t stream);
+
+/* Per-kernel timing for the benchmark's roofline: between nw_profile_begin()
+ * and nw_profile_end() every library launch is bracketed by CUDA events on its
+ * stream.  nw_profile_end synchronises those events and writes, for up to
+ * `cap` kernel kinds, the kind name (static string), launch count and total
+ * milliseconds; *n receives the number of kinds.  Not thread-safe. */
+NW_API nw_status_t nw_profile_begin(void);
+NW_API nw_status_t nw_profile_end(const char **names, unsigned long long *launches, double *ms,
+                                  size_t cap, size_t *n);
+
 /* EWMM multiplications of one nested forward (slices * P * Cin_e * Cout_e). */
 NW_API nw_status_t nw_count_mults(nw_plan_t plan, int N, int H, int W, unsigned long long *ewmm);
 

@@ -26,7 +26,8 @@ EXPORTS = [
     "nw_plan", "nw_plan_set", "nw_plan_set_prelu", "nw_plan_finalize", "nw_plan_destroy", "nw_plan_info",
     "nw_plan_tables", "nw_output_size", "nw_workspace_size", "nw_workspace_size_ola",
     "nw_workspace_size_direct", "nw_transform_filter", "nw_conv_forward", "nw_conv_ola", "nw_conv_direct",
-    "nw_count_mults", "nw_launch_count", "nw_status_str",
+    "nw_count_mults", "nw_launch_count", "nw_status_str", "nw_workspace_size_host", "nw_conv_forward_host",
+    "nw_profile_begin", "nw_profile_end",
 ]
 
 
@@ -79,6 +80,11 @@ def load() -> ctypes.CDLL:
         "nw_count_mults": (st, [P, I, I, I, ctypes.POINTER(ctypes.c_ulonglong)]),
         "nw_launch_count": (ctypes.c_ulonglong, []),
         "nw_status_str": (ctypes.c_char_p, [I]),
+        "nw_workspace_size_host": (st, [P, I, I, I, ctypes.POINTER(SZ)]),
+        "nw_conv_forward_host": (st, [P, VP, VP, VP, I, I, I, VP, SZ, VP]),
+        "nw_profile_begin": (st, []),
+        "nw_profile_end": (st, [ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_ulonglong),
+                                ctypes.POINTER(ctypes.c_double), SZ, ctypes.POINTER(SZ)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -166,7 +172,7 @@ class Plan:
     def workspace_size(self, N: int, H: int, W: int, path: str = "nested") -> int:
         lib = load()
         fn = {"nested": lib.nw_workspace_size, "ola": lib.nw_workspace_size_ola,
-              "direct": lib.nw_workspace_size_direct}[path]
+              "direct": lib.nw_workspace_size_direct, "host": lib.nw_workspace_size_host}[path]
         b = ctypes.c_size_t()
         _chk(fn(self._h, N, H, W, ctypes.byref(b)), f"workspace_size({path})")
         return b.value
@@ -183,6 +189,11 @@ class Plan:
         _chk(load().nw_conv_forward(self._h, _ptr(x), _ptr(U), _ptr(y), N, H, W, _ptr(ws), ws_bytes,
                                     _stream(stream)), "nw_conv_forward")
 
+    def forward_host(self, x_host, U, y_host, N: int, H: int, W: int, ws, ws_bytes: int, stream=None) -> None:
+        """x_host / y_host: host (ideally pinned) tensors; copies happen inside the call."""
+        _chk(load().nw_conv_forward_host(self._h, _ptr(x_host), _ptr(U), _ptr(y_host), N, H, W, _ptr(ws),
+                                         ws_bytes, _stream(stream)), "nw_conv_forward_host")
+
     def ola(self, x, w, y, N: int, H: int, W: int, ws, ws_bytes: int, stream=None) -> None:
         _chk(load().nw_conv_ola(self._h, _ptr(x), _ptr(w), _ptr(y), N, H, W, _ptr(ws), ws_bytes,
                                 _stream(stream)), "nw_conv_ola")
@@ -194,3 +205,19 @@ class Plan:
 
 def launch_count() -> int:
     return int(load().nw_launch_count())
+
+
+def profile_begin() -> None:
+    _chk(load().nw_profile_begin(), "nw_profile_begin")
+
+
+def profile_end() -> dict:
+    """{kernel kind: (launches, total ms)} for launches since profile_begin()."""
+    lib = load()
+    cap = 32
+    names = (ctypes.c_char_p * cap)()
+    cnt = (ctypes.c_ulonglong * cap)()
+    ms = (ctypes.c_double * cap)()
+    n = ctypes.c_size_t()
+    _chk(lib.nw_profile_end(names, cnt, ms, cap, ctypes.byref(n)), "nw_profile_end")
+    return {names[i].decode(): (int(cnt[i]), float(ms[i])) for i in range(min(n.value, cap))}

@@ -44,3 +44,42 @@ nw_status_t nw_conv_forward(nw_plan_t p, const void *x, const void *U, void *y, 
 }
 
 }  // extern "C"
+
+extern "C" {
+
+nw_status_t nw_workspace_size_host(nw_plan_t p, int N, int H, int W, size_t *bytes) {
+  size_t b = 0;
+  nw_status_t st = nw_workspace_size(p, N, H, W, &b);
+  if (st != NW_OK) return st;
+  Geometry g = make_geometry(p, N, H, W);
+  const size_t es = (p->dtype == NW_DTYPE_BF16) ? 2 : 4;
+  const size_t xb = (size_t)round_up((long long)N * p->Cin * H * W * es, 256);
+  const size_t yb = (size_t)round_up((long long)N * p->Cout * g.Ho * g.Wo * es, 256);
+  *bytes = b + xb + yb;
+  return NW_OK;
+}
+
+nw_status_t nw_conv_forward_host(nw_plan_t p, const void *x_host, const void *U, void *y_host, int N, int H, int W,
+                                 void *ws, size_t ws_bytes, nw_stream_t stream) {
+  if (!p || !x_host || !y_host || !U || N < 1 || H < 1 || W < 1) return NW_ERR_INVALID;
+  size_t need = 0;
+  nw_status_t st = nw_workspace_size_host(p, N, H, W, &need);
+  if (st != NW_OK) return st;
+  if (!ws || ws_bytes < need) return NW_ERR_WORKSPACE;
+  Geometry g = make_geometry(p, N, H, W);
+  const size_t es = (p->dtype == NW_DTYPE_BF16) ? 2 : 4;
+  const size_t xbytes = (size_t)N * p->Cin * H * W * es;
+  const size_t ybytes = (size_t)N * p->Cout * g.Ho * g.Wo * es;
+  const size_t fw = v_bytes(p, g) + m_bytes(p, g);
+  char *base = static_cast<char *>(ws);
+  char *xd = base + fw;
+  char *yd = xd + (size_t)round_up((long long)xbytes, 256);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(xd, x_host, xbytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return NW_ERR_CUDA;
+  st = nw_conv_forward(p, xd, U, yd, N, H, W, ws, fw, stream);
+  if (st != NW_OK) return st;
+  if (cudaMemcpyAsync(y_host, yd, ybytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) return NW_ERR_CUDA;
+  return NW_OK;
+}
+
+}  // extern "C"

@@ -81,6 +81,7 @@ nw_status_t launch_filter_transform(const nw_plan_st* p, const Geometry& g, cons
   const long long n = (long long)g.cout_pad * g.cin_pad;
   const int blocks = (int)((n + 127) / 128);
   const bool bf = p->math != NW_MATH_FP32_SIMT;
+  LaunchScope scope_("filter_transform", s);
   if (p->dtype == NW_DTYPE_BF16) {
     const __nv_bfloat16* wb = static_cast<const __nv_bfloat16*>(w);
     if (bf) filter_transform_kernel<__nv_bfloat16, true><<<blocks, 128, 0, s>>>(wb, U, g, p->K, G);

@@ -54,6 +54,7 @@ nw_status_t launch_gemm_simt(const nw_plan_st* p, const Geometry& g, const float
                              cudaStream_t s) {
   (void)p;
   dim3 grid((unsigned)(g.T_pad / 64), (unsigned)((g.cout_pad + 63) / 64), (unsigned)g.P);
+  LaunchScope scope_("contraction_fp32_simt", s);
   gemm_simt_kernel<<<grid, 256, 0, s>>>(V, U, M, g.T_pad, g.cin_pad, g.cout_pad);
   return check_launch();
 }

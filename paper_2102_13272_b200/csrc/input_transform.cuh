@@ -148,6 +148,7 @@ static nw_status_t input_launch(const Geometry& g, const void* x, void* V, cudaS
   const long long gx = (long long)g.N * g.tiles_h * wgroups;
   const int cin_src = (SR == 1) ? g.cin_pad : g.cin_pad / 4;
   dim3 grid((unsigned)gx, (unsigned)((cin_src + C::CC - 1) / C::CC));
+  LaunchScope scope_("input_transform", s);
   kern<<<grid, 256, C::SMEM, s>>>(static_cast<const XT*>(x), V, g);
   return check_launch();
 }

@@ -72,6 +72,20 @@ nw_status_t launch_gemm_simt(const nw_plan_st *p, const Geometry &g, const float
 nw_status_t launch_gemm_tc(const nw_plan_st *p, const Geometry &g, const void *V, const void *U,
                            float *M, cudaStream_t s);
 
+// RAII: when profiling is on, brackets one launch with CUDA events on its stream.
+class LaunchScope {
+ public:
+  LaunchScope(const char *kind, cudaStream_t s);
+  ~LaunchScope();
+  LaunchScope(const LaunchScope &) = delete;
+  LaunchScope &operator=(const LaunchScope &) = delete;
+
+ private:
+  const char *kind_;
+  cudaStream_t s_;
+  cudaEvent_t a_ = nullptr, b_ = nullptr;
+};
+
 inline nw_status_t check_launch() {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError() == cudaSuccess ? NW_OK : NW_ERR_CUDA;

@@ -126,6 +126,7 @@ static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const f
   const int wgroups = (g.tiles_w + C::TWO - 1) / C::TWO;
   const long long gx = (long long)g.N * g.tiles_h * wgroups;
   dim3 grid((unsigned)gx, (unsigned)((g.cout_e + C::CO - 1) / C::CO));
+  LaunchScope scope_("output_transform", s);
   kern<<<grid, 256, C::SMEM, s>>>(M, static_cast<YT*>(y), g, p->prelu ? p->slopes : nullptr);
   return check_launch();
 }
