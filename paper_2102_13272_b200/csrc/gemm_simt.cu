@@ -5,7 +5,7 @@ namespace nw {
 
 // ---------------------------------------------------------------------------
 // G3s: FP32 SIMT contraction, batched over transform points
-// M[xi][t][co] = sum_k V[xi][t][k] * U[xi][co][k]
+// M[xi][co][t] = sum_k V[xi][t][k] * U[xi][co][k]
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict__ V, const float* __restrict__ U,
                                                         float* __restrict__ M, long long T_pad, int K, int Nn) {
@@ -40,12 +40,13 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
     }
     __syncthreads();
   }
+  // M layout [xi][co][t]: four consecutive slices per float4
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const long long t = t0 + ty * 4 + i;
-    float* dst = M + ((long long)xi * T_pad + t) * Nn + n0 + tx * 4;
-    if (n0 + tx * 4 + 3 < Nn) {
-      *reinterpret_cast<float4*>(dst) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+  for (int j = 0; j < 4; ++j) {
+    const int co = n0 + tx * 4 + j;
+    if (co < Nn) {
+      float* dst = M + ((long long)xi * Nn + co) * T_pad + t0 + ty * 4;
+      *reinterpret_cast<float4*>(dst) = make_float4(acc[0][j], acc[1][j], acc[2][j], acc[3][j]);
     }
   }
 }

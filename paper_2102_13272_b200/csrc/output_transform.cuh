@@ -1,117 +1,128 @@
-// output_transform.cuh -- G4 kernel template (instantiated per axis combo in output_*.cu)
+// output_transform.cuh -- G4: nested output transform fused with the store.
+// Instantiated per axis combo in xform_*.cu.
+//
+// M layout [P][cout_pad][T_pad] (fp32): one warp owns 32 consecutive slices of one
+// output channel, so every load of M is a 128-byte coalesced row.  Each thread
+// keeps the 9x9 (M_a x M_a) output tile of its slice in registers: for each
+// point row p_h it applies A^T_hat along w (factored, 25 -> 9) and accumulates
+// A^T_hat[q_h][p_h] times that row into the tile (composite along h, zero
+// coefficients skipped at compile time).  The tile then goes through a per-warp
+// shared-memory stage so the stores walk whole output rows across the 32 slices
+// (adjacent tiles are adjacent in w), applying the keep mask (redundant terms /
+// coverage phases), the crop, the transposed-conv depth-to-space, PReLU and the
+// dtype cast.
 #pragma once
 #include "transforms.cuh"
 
 namespace nw {
 
-// ---------------------------------------------------------------------------
-// G4: output transform + keep/crop + (depth-to-space) + PReLU + store
-// Block = (n, a_h, TWO tiles along w) x CO output channels (of Cout_e).
-// ---------------------------------------------------------------------------
+struct AtHatF {
+  float a[kMaxMa][kMaxPa];
+};
+template <int MO, int RO, int MI>
+__host__ __device__ constexpr AtHatF make_athat() {
+  AtHatF T{};
+  NestedAxis A = make_axis(MO, RO, MI);
+  for (int q = 0; q < A.Ma; ++q)
+    for (int p = 0; p < A.Pa; ++p) T.a[q][p] = float(rdouble(at_hat(A, q, p)));
+  return T;
+}
+
 template <int MO, int RO, int MI>
 struct OutCfg {
   using X = Ax<MO, RO, MI>;
-  static constexpr int CO = 16, TWO = 4;
-  static constexpr int QS = TWO * X::PA * X::MA * CO;
-  static constexpr int YW = TWO * X::ADV;
-  static constexpr int YS = CO * X::ADV * YW;
-  static constexpr size_t SMEM = (size_t)(QS + YS) * sizeof(float);
+  static constexpr int WARPS = 8;
+  static constexpr int STAGE = 32 * X::MA * X::MA + 1;  // floats per warp (odd stride per slice)
+  static constexpr size_t SMEM = (size_t)WARPS * STAGE * sizeof(float);
 };
 
 template <int MO, int RO, int MI, typename YT>
-__global__ void __launch_bounds__(256) output_transform_kernel(const float* __restrict__ M, YT* __restrict__ y,
-                                                               Geometry g, const float* __restrict__ slopes) {
+__global__ void __launch_bounds__(256, 2) output_transform_kernel(const float* __restrict__ M, YT* __restrict__ y,
+                                                                  Geometry g, const float* __restrict__ slopes) {
   using X = Ax<MO, RO, MI>;
   using C = OutCfg<MO, RO, MI>;
   constexpr NestedAxis A = make_axis(MO, RO, MI);
+  constexpr AtHatF AT = make_athat<MO, RO, MI>();
+  constexpr int MA = X::MA, PA = X::PA, NPH = X::NPH;
   extern __shared__ __align__(16) float smem[];
-  float* Qs = smem;
-  float* Ys = smem + C::QS;
-  const int tid = threadIdx.x;
-  const int wgroups = (g.tiles_w + C::TWO - 1) / C::TWO;
-  int b = blockIdx.x;
-  const int wg = b % wgroups;
-  b /= wgroups;
-  const int ah = b % g.tiles_h;
-  const int n = b / g.tiles_h;
-  const int co0 = blockIdx.y * C::CO;
-  const int aw0 = wg * C::TWO;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* stage = smem + warp * C::STAGE;
 
+  const long long t0 = (long long)blockIdx.x * 32;
+  const int coe = blockIdx.y * C::WARPS + warp;
+  if (coe >= g.cout_e) return;
+  const long long t = t0 + lane;
+  const bool valid = t < g.T;
+
+  float Y[MA][MA];
 #pragma unroll
-  for (int ph = 0; ph < X::NPH; ++ph) {
+  for (int i = 0; i < MA; ++i)
 #pragma unroll
-    for (int pw = 0; pw < X::NPH; ++pw) {
-      __syncthreads();
-      // pass A: along w, Q[tile][p_h][q_w][co]
-      for (int task = tid; task < C::CO * C::TWO * X::PA; task += blockDim.x) {
-        const int co = task % C::CO;
-        const int tile = (task / C::CO) % C::TWO;
-        const int p_h = task / (C::CO * C::TWO);
-        const int aw = aw0 + tile;
-        float mv[X::PA], qv[X::MA];
-        if (aw < g.tiles_w) {
-          const long long t = ((((long long)n * g.tiles_h + ah) * g.tiles_w + aw) * X::NPH + ph) * X::NPH + pw;
-          const float* src = M + ((long long)(p_h * X::PA) * g.T_pad + t) * g.cout_pad + co0 + co;
-          const long long step = (long long)g.T_pad * g.cout_pad;
+    for (int j = 0; j < MA; ++j) Y[i][j] = 0.f;
+
+  const long long pstride = (long long)g.cout_pad * g.T_pad;   // between consecutive points
+  const float* src = M + (long long)coe * g.T_pad + (valid ? t : 0);
 #pragma unroll
-          for (int p_w = 0; p_w < X::PA; ++p_w) mv[p_w] = __ldg(src + p_w * step);
-        } else {
+  for (int p_h = 0; p_h < PA; ++p_h) {
+    float mv[PA], qv[MA];
 #pragma unroll
-          for (int p_w = 0; p_w < X::PA; ++p_w) mv[p_w] = 0.f;
-        }
-        out_axis<MO, RO, MI>(mv, qv);
+    for (int p_w = 0; p_w < PA; ++p_w) mv[p_w] = __ldg(src + (long long)(p_h * PA + p_w) * pstride);
+    out_axis<MO, RO, MI>(mv, qv);
 #pragma unroll
-        for (int q = 0; q < X::MA; ++q) Qs[((tile * X::PA + p_h) * X::MA + q) * C::CO + co] = qv[q];
-      }
-      __syncthreads();
-      // pass B: along h, scatter kept outputs into Ys[co][i][tile*adv + j]
-      for (int task = tid; task < C::CO * C::TWO * X::MA; task += blockDim.x) {
-        const int co = task % C::CO;
-        const int tile = (task / C::CO) % C::TWO;
-        const int q_w = task / (C::CO * C::TWO);
-        if (!keep(A, pw, q_w)) continue;
-        float mv[X::PA], yv[X::MA];
+    for (int q_h = 0; q_h < MA; ++q_h) {
+      if (AT.a[q_h][p_h] != 0.f) {
 #pragma unroll
-        for (int p_h = 0; p_h < X::PA; ++p_h) mv[p_h] = Qs[((tile * X::PA + p_h) * X::MA + q_w) * C::CO + co];
-        out_axis<MO, RO, MI>(mv, yv);
-        const int jw = tile * X::ADV + A.shift[pw] + out_pos(A, q_w);
-#pragma unroll
-        for (int q_h = 0; q_h < X::MA; ++q_h) {
-          if (keep(A, ph, q_h)) {
-            const int ih = A.shift[ph] + out_pos(A, q_h);
-            Ys[(co * X::ADV + ih) * C::YW + jw] = yv[q_h];
-          }
-        }
+        for (int q_w = 0; q_w < MA; ++q_w) Y[q_h][q_w] = fmaf(AT.a[q_h][p_h], qv[q_w], Y[q_h][q_w]);
       }
     }
   }
-  __syncthreads();
-  // cooperative store (rows of TWO*adv consecutive outputs)
-  for (int idx = tid; idx < C::CO * X::ADV * C::YW; idx += blockDim.x) {
-    const int j = idx % C::YW;
-    const int i = (idx / C::YW) % X::ADV;
-    const int co = idx / (C::YW * X::ADV);
-    const int coe = co0 + co;
-    if (coe >= g.cout_e) continue;
-    const int gi = ah * X::ADV + i, gj = aw0 * X::ADV + j;
+
+  // stage the tile: stage[lane * MA*MA + q_h*MA + q_w]
+#pragma unroll
+  for (int q_h = 0; q_h < MA; ++q_h)
+#pragma unroll
+    for (int q_w = 0; q_w < MA; ++q_w) stage[lane * (MA * MA) + q_h * MA + q_w] = Y[q_h][q_w];
+  __syncwarp();
+
+  // store: index = (q_h, slice, q_w) so consecutive lanes walk one output row across slices
+  int c = coe, fo_h = 0, fo_w = 0;
+  if (g.mode == 2) {
+    const int f = coe / g.Cout;
+    c = coe % g.Cout;
+    fo_h = f / 2;
+    fo_w = f % 2;
+  }
+  const float slope = slopes ? slopes[c] : 0.f;
+  const long long nslices = g.T - t0 < 32 ? g.T - t0 : 32;
+  for (int idx = lane; idx < 32 * MA * MA; idx += 32) {
+    const int q_w = idx % MA;
+    const int s = (idx / MA) % 32;
+    const int q_h = idx / (MA * 32);
+    if (s >= nslices) continue;
+    long long ts = t0 + s;
+    const int phw = (int)(ts % NPH);
+    ts /= NPH;
+    const int phh = (int)(ts % NPH);
+    ts /= NPH;
+    const int aw = (int)(ts % g.tiles_w);
+    ts /= g.tiles_w;
+    const int ah = (int)(ts % g.tiles_h);
+    const int n = (int)(ts / g.tiles_h);
+    if (!keep(A, phh, q_h) || !keep(A, phw, q_w)) continue;
+    const int gi = ah * X::ADV + A.shift[phh] + out_pos(A, q_h);
+    const int gj = aw * X::ADV + A.shift[phw] + out_pos(A, q_w);
     if (gi >= g.Hq || gj >= g.Wq) continue;
-    int c = coe, Y = gi, Xc = gj;
+    int Yr = gi, Xc = gj;
     if (g.mode == 2) {
-      const int f = coe / g.Cout;
-      c = coe % g.Cout;
-      Y = 2 * gi + f / 2;
-      Xc = 2 * gj + f % 2;
+      Yr = 2 * gi + fo_h;
+      Xc = 2 * gj + fo_w;
+      if (Yr >= g.Ho || Xc >= g.Wo) continue;
     }
-    if (Y >= g.Ho || Xc >= g.Wo) continue;
-    float v = Ys[idx];
-    if (slopes) v = v >= 0.f ? v : slopes[c] * v;
-    y[(((long long)n * g.Cout + c) * g.Ho + Y) * g.Wo + Xc] = from_f<YT>(v);
+    float v = stage[s * (MA * MA) + q_h * MA + q_w];
+    if (slopes) v = v >= 0.f ? v : slope * v;
+    y[(((long long)n * g.Cout + c) * g.Ho + Yr) * g.Wo + Xc] = from_f<YT>(v);
   }
 }
-
-}  // namespace nw
-
-namespace nw {
 
 template <int MO, int RO, int MI, typename YT>
 static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const float* M, void* y, cudaStream_t s) {
@@ -123,11 +134,9 @@ static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const f
       return NW_ERR_CUDA;
     attr_done = true;
   }
-  const int wgroups = (g.tiles_w + C::TWO - 1) / C::TWO;
-  const long long gx = (long long)g.N * g.tiles_h * wgroups;
-  dim3 grid((unsigned)gx, (unsigned)((g.cout_e + C::CO - 1) / C::CO));
+  dim3 grid((unsigned)((g.T + 31) / 32), (unsigned)((g.cout_e + C::WARPS - 1) / C::WARPS));
   LaunchScope scope_("output_transform", s);
-  kern<<<grid, 256, C::SMEM, s>>>(M, static_cast<YT*>(y), g, p->prelu ? p->slopes : nullptr);
+  kern<<<grid, 32 * C::WARPS, C::SMEM, s>>>(M, static_cast<YT*>(y), g, p->prelu ? p->slopes : nullptr);
   return check_launch();
 }
 

@@ -1,8 +1,367 @@
-// tc_gemm.cu -- tcgen05 contraction (placeholder until the kernel lands).
+// tc_gemm.cu -- G3: the per-transform-point channel contraction on 5th-gen tensor
+// cores (tcgen05, sm_100a).  For every point xi of the P = P_a^2 transform points
+//     M_xi[T x Cout_e] = V_xi[T x Cin_e] . U_xi[Cout_e x Cin_e]^T
+// (the EWMM of P:110 summed over input channels, Eq. 2.1), the only dense
+// contraction of the method.
+//
+// Precision (R12): BF16X3 splits both operands into bf16 hi/lo planes
+// (written by the input / filter transforms) and issues three kind::f16 MMAs per
+// K step into one fp32 TMEM accumulator: Vh.Uh + Vh.Ul + Vl.Uh.  BF16 issues Vh.Uh.
+//
+// Structure (persistent, warp-specialised, 1 CTA per SM):
+//   warp 0 lane 0  TMA producer: B ring (U_xi k-block, hi+lo) and A ring (128-slice
+//                  blocks of V_xi, hi+lo), 128B-swizzled, mbarrier complete_tx
+//   warp 1 lane 0  MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128, N=Cout_pad,
+//                  K=16 per instruction, accumulators double-buffered in TMEM,
+//                  tcgen05.commit frees smem stages / signals the epilogue
+//   warps 2..5     epilogue: tcgen05.ld 32x32b -> registers -> coalesced stores of
+//                  M[xi][co][t] (each warp owns a 32-lane TMEM quarter = 32 slices)
+// A work unit is (xi, group of G 128-slice blocks); one B k-block is loaded per
+// unit and k-block and reused by the G A blocks (G*N <= 256 TMEM columns).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
 #include "nw_internal.h"
 
 namespace nw {
-nw_status_t launch_gemm_tc(const nw_plan_st *, const Geometry &, const void *, const void *, float *, cudaStream_t) {
-  return NW_ERR_UNSUPPORTED;
+namespace tc {
+
+constexpr int kBM = 128;      // slices per MMA (TMEM lanes)
+constexpr int kBK = 64;       // bf16 elements per 128-byte swizzle row
+constexpr int kThreads = 192;
+constexpr int kMaxStages = 8;
+
+// ------------------------------- PTX wrappers --------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t"
+      "}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address >> 4
+  d |= (uint64_t)(0) << 16;                         // leading byte offset (unused for K-major SW128)
+  d |= (uint64_t)((1024 >> 4) & 0x3FFF) << 32;      // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                           // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                           // layout: SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor: D fp32, A/B bf16, both K-major, M=128, N=n.
+__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+}
+
+struct Params {
+  int P;            // transform points
+  int nmb;          // 128-slice blocks per point (T_pad / 128)
+  int G;            // blocks per unit
+  int ngrp;         // unit groups per point = ceil(nmb / G)
+  int N;            // cout_pad (MMA N, <= 256)
+  int KB;           // k-blocks of 64 (ceil(cin_pad / 64))
+  int lo;           // 1 = bf16x3 (lo planes), 0 = plain bf16
+  int nA, nB;       // ring depths
+  long long T_pad;
+  long long a_lo_row; // row offset of the lo plane in the V tensor map (= P * T_pad)
+  long long b_lo_row; // row offset of the lo plane in the U tensor map (= P * N)
+  float* M;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    contraction_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapU,
+                       const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the swizzled tiles
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* sbase = smem_raw + (base - raw);
+
+  const uint32_t a_plane = kBM * kBK * 2;              // 16 KB
+  const uint32_t a_stage = a_plane * (p.lo ? 2 : 1);
+  const uint32_t b_plane = (uint32_t)p.N * kBK * 2;    // N x 128 B
+  const uint32_t b_stage = b_plane * (p.lo ? 2 : 1);
+  const uint32_t a_off = 0;
+  const uint32_t b_off = a_off + a_stage * p.nA;
+  const uint32_t bar_off = b_off + b_stage * p.nB;
+  // barriers: A_full[nA], A_empty[nA], B_full[nB], B_empty[nB], T_full[2], T_empty[2], tmem addr
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + bar_off);
+  uint64_t* A_full = bars;
+  uint64_t* A_empty = bars + kMaxStages;
+  uint64_t* B_full = bars + 2 * kMaxStages;
+  uint64_t* B_empty = bars + 3 * kMaxStages;
+  uint64_t* T_full = bars + 4 * kMaxStages;
+  uint64_t* T_empty = bars + 4 * kMaxStages + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * kMaxStages + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total_units = p.P * p.ngrp;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapV);
+    tma_prefetch(&mapU);
+    for (int i = 0; i < p.nA; ++i) { mbar_init(smem_u32(&A_full[i]), 1); mbar_init(smem_u32(&A_empty[i]), 1); }
+    for (int i = 0; i < p.nB; ++i) { mbar_init(smem_u32(&B_full[i]), 1); mbar_init(smem_u32(&B_empty[i]), 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(smem_u32(&T_full[i]), 1); mbar_init(smem_u32(&T_empty[i]), 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // whole warp allocates TMEM (512 columns: 2 accumulator buffers)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------ TMA producer ------------------------------
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+        const int xi = u / p.ngrp, grp = u % p.ngrp;
+        const int mb0 = grp * p.G;
+        const int g_eff = min(p.G, p.nmb - mb0);
+        for (int kb = 0; kb < p.KB; ++kb) {
+          mbar_wait(smem_u32(&B_empty[sb]), pb ^ 1);
+          const uint32_t bfull = smem_u32(&B_full[sb]);
+          mbar_expect_tx(bfull, b_stage);
+          const uint32_t bdst = base + b_off + sb * b_stage;
+          tma_load_2d(bdst, &mapU, bfull, kb * kBK, xi * p.N);
+          if (p.lo) tma_load_2d(bdst + b_plane, &mapU, bfull, kb * kBK, (int)(p.b_lo_row + (long long)xi * p.N));
+          if (++sb == p.nB) { sb = 0; pb ^= 1; }
+          for (int g = 0; g < g_eff; ++g) {
+            mbar_wait(smem_u32(&A_empty[sa]), pa ^ 1);
+            const uint32_t afull = smem_u32(&A_full[sa]);
+            mbar_expect_tx(afull, a_stage);
+            const uint32_t adst = base + a_off + sa * a_stage;
+            const long long row = (long long)xi * p.T_pad + (long long)(mb0 + g) * kBM;
+            tma_load_2d(adst, &mapV, afull, kb * kBK, (int)row);
+            if (p.lo) tma_load_2d(adst + a_plane, &mapV, afull, kb * kBK, (int)(p.a_lo_row + row));
+            if (++sa == p.nA) { sa = 0; pa ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------- MMA issuer -------------------------------
+      const uint32_t idesc = idesc_bf16(p.N);
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      int it = 0;
+      for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++it) {
+        const int grp = u % p.ngrp;
+        const int g_eff = min(p.G, p.nmb - grp * p.G);
+        const int buf = it & 1;
+        const uint32_t tpar = (uint32_t)((it >> 1) & 1);
+        mbar_wait(smem_u32(&T_empty[buf]), tpar ^ 1);
+        fence_after();
+        const uint32_t acc0 = tmem_base + (uint32_t)(buf * 256);
+        for (int kb = 0; kb < p.KB; ++kb) {
+          mbar_wait(smem_u32(&B_full[sb]), pb);
+          const uint32_t bsm = base + b_off + sb * b_stage;
+          for (int g = 0; g < g_eff; ++g) {
+            mbar_wait(smem_u32(&A_full[sa]), pa);
+            fence_after();
+            const uint32_t asm_ = base + a_off + sa * a_stage;
+            const uint32_t acc = acc0 + (uint32_t)(g * p.N);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t ah = sw128_desc(asm_ + k * 32);
+              const uint64_t bh = sw128_desc(bsm + k * 32);
+              const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+              umma_f16(acc, ah, bh, idesc, accum);
+              if (p.lo) {
+                const uint64_t al = sw128_desc(asm_ + a_plane + k * 32);
+                const uint64_t bl = sw128_desc(bsm + b_plane + k * 32);
+                umma_f16(acc, ah, bl, idesc, 1u);
+                umma_f16(acc, al, bh, idesc, 1u);
+              }
+            }
+            umma_commit(smem_u32(&A_empty[sa]));
+            if (++sa == p.nA) { sa = 0; pa ^= 1; }
+          }
+          umma_commit(smem_u32(&B_empty[sb]));
+          if (++sb == p.nB) { sb = 0; pb ^= 1; }
+        }
+        umma_commit(smem_u32(&T_full[buf]));
+      }
+    }
+  } else {
+    // -------------------------------- epilogue ---------------------------------
+    const int quarter = warp & 3;                     // TMEM lanes [32q, 32q+32)
+    const int row = quarter * 32 + lane;
+    int it = 0;
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++it) {
+      const int xi = u / p.ngrp, grp = u % p.ngrp;
+      const int mb0 = grp * p.G;
+      const int g_eff = min(p.G, p.nmb - mb0);
+      const int buf = it & 1;
+      const uint32_t tpar = (uint32_t)((it >> 1) & 1);
+      mbar_wait(smem_u32(&T_full[buf]), tpar);
+      fence_after();
+      for (int g = 0; g < g_eff; ++g) {
+        const long long t = (long long)(mb0 + g) * kBM + row;
+        float* dst = p.M + (long long)xi * p.N * p.T_pad + t;
+        for (int c0 = 0; c0 < p.N; c0 += 16) {
+          uint32_t r[16];
+          const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * 256 + g * p.N + c0);
+          tmem_ld16(taddr, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) dst[(long long)(c0 + j) * p.T_pad] = __uint_as_float(r[j]);
+        }
+      }
+      fence_before();
+      mbar_arrive(smem_u32(&T_empty[buf]));
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u));
+}
+
+}  // namespace tc
+
+// ------------------------------ host side ------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map [rows][cols] with a (64 x box_rows) box, 128-byte swizzle.
+static bool make_map(CUtensorMap* m, const void* base, long long rows, long long cols, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)tc::kBK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V, const void* U, float* M,
+                           cudaStream_t s) {
+  if (g.cout_pad > 256) return NW_ERR_UNSUPPORTED;
+  tc::Params prm{};
+  prm.P = g.P;
+  prm.nmb = (int)(g.T_pad / tc::kBM);
+  prm.N = g.cout_pad;
+  prm.G = 256 / prm.N;
+  if (prm.G > 4) prm.G = 4;
+  if (prm.G < 1) prm.G = 1;
+  prm.ngrp = (prm.nmb + prm.G - 1) / prm.G;
+  prm.KB = (g.cin_pad + tc::kBK - 1) / tc::kBK;
+  prm.lo = (p->math == NW_MATH_BF16X3) ? 1 : 0;
+  prm.T_pad = g.T_pad;
+  prm.a_lo_row = (long long)g.P * g.T_pad;
+  prm.b_lo_row = (long long)g.P * g.cout_pad;
+  prm.M = M;
+  const uint32_t a_stage = tc::kBM * tc::kBK * 2 * (prm.lo ? 2 : 1);
+  const uint32_t b_stage = (uint32_t)prm.N * tc::kBK * 2 * (prm.lo ? 2 : 1);
+  // ring depths within ~200 KB
+  const uint32_t budget = 200 * 1024;
+  prm.nB = 2;
+  prm.nA = (int)((budget - prm.nB * b_stage) / a_stage);
+  if (prm.nA > 6) prm.nA = 6;
+  if (prm.nA < 2) {
+    prm.nB = 1;
+    prm.nA = (int)((budget - b_stage) / a_stage);
+    if (prm.nA < 2) return NW_ERR_UNSUPPORTED;
+  }
+  size_t smem = 1024 + (size_t)a_stage * prm.nA + (size_t)b_stage * prm.nB + (4 * tc::kMaxStages + 8) * 8;
+  if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM: each CTA owns all 512 TMEM columns
+  const long long rowsV = (long long)g.P * g.T_pad * (prm.lo ? 2 : 1);
+  const long long rowsU = (long long)g.P * g.cout_pad * (prm.lo ? 2 : 1);
+  if (rowsV >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
+  alignas(64) CUtensorMap mapV, mapU;
+  if (!make_map(&mapV, V, rowsV, g.cin_pad, tc::kBM)) return NW_ERR_CUDA;
+  if (!make_map(&mapU, U, rowsU, g.cin_pad, prm.N)) return NW_ERR_CUDA;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(tc::contraction_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+        cudaSuccess)
+      return NW_ERR_CUDA;
+    attr = true;
+  }
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long units = (long long)prm.P * prm.ngrp;
+  const int grid = (int)(units < sms ? units : sms);
+  LaunchScope scope_("contraction_tc", s);
+  tc::contraction_kernel<<<grid, tc::kThreads, smem, s>>>(mapV, mapU, prm);
+  return check_launch();
+}
+
 }  // namespace nw
