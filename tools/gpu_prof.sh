@@ -1,0 +1,17 @@
+# usage: bash tools/gpu_prof.sh <tag> <layer>  -- bench line, launch list and ncu --set full of the 3 kernels
+set -x
+TAG=${1:-r1}
+LAYER=${2:-c2k9}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap --format=csv -lms 200 > gpurun_out/clocks_$TAG.csv &
+SMI=$!
+timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"
+kill $SMI
+timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-compare > gpurun_out/plain_$TAG.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
+  python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-compare > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "launches rc=$?"
+timeout 300 python tools/prof_layer.py $LAYER > gpurun_out/prof_plain_$TAG.log 2>&1 && \
+for K in input_transform contraction output_transform; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 \
+    -o gpurun_out/prof_${TAG}_${LAYER}_$K python tools/prof_layer.py $LAYER > gpurun_out/ncu_${K}_$TAG.log 2>&1; echo "ncu $K rc=$?"
+done
