@@ -1,143 +1,187 @@
-// input_transform.cuh -- G2 kernel template (instantiated per axis combo in input_*.cu)
+// input_transform.cuh -- G2: nested input transform V = B^T_hat X B_hat.
+// Instantiated per axis combo in xform_*.cu.
+//
+// Block = (image n, tile row a_h, TW adjacent tiles along w) x CC source
+// channels; the channel group is the fastest grid index so the blocks that fill
+// one 128-byte V row run together.  256 threads, two passes over shared memory:
+//   pass 1  thread = (channel, raw window column): the SR*(shift_max + L) window
+//           rows are read straight from x (coalesced along w, zero outside the
+//           image = the padding), B^T_hat is applied along h per stride phase
+//           p and coverage phase, the P_a results go to Hs[ph][p][p_h][c][col].
+//   pass 2  thread = (channel pair, tile, p_h): two L-long rows of Hs are
+//           transformed along w; each of the P_a outputs is split into bf16
+//           hi/lo (one cvt.rn.bf16x2 per pair and plane) and the pair is stored
+//           with one 4-byte store per plane (fp32 path: one 8-byte store).
+// A "pair" is two adjacent contraction channels ce: source channels (2k, 2k+1)
+// at stride 1, the two column phases q = 0, 1 of one (channel, row phase) at
+// stride 2 (ce = 4 ci + 2 p + q, Eq. 2.7 folded into K, R9).
+// Channels >= Cin (up to cin_pad) are written as zeros: the contraction runs
+// over cin_pad.
 #pragma once
 #include "transforms.cuh"
 
 namespace nw {
 
-// ---------------------------------------------------------------------------
-// G2: input transform
-// Block = (n, tile row a_h, TW tiles along w) x CC input channels.  The input
-// region (rows of every coverage / stride phase, TW slice windows) is staged in
-// shared memory [row][col][cc] (zero-filled outside the image = the padding).
-// Pass 1 transforms every staged column along h (B^T_hat on rows) into
-// Hs[p_h][col][cc]; pass 2 transforms along w per (tile, p_h) and stores the
-// P_a values of V[xi = p_h*P_a + p_w][t][ce].  With bf16 output each lane pair
-// exchanges (hi, lo) so one lane writes the hi plane pair and the other the lo
-// plane pair (4-byte stores, full 32-byte sectors per 8 lanes).
-// ---------------------------------------------------------------------------
-template <int MO, int RO, int MI, int SR>
+template <int MO, int RO, int MI, int SR, int CC>
 struct InCfg {
   using X = Ax<MO, RO, MI>;
-  static constexpr int CC = (SR == 1) ? 16 : 8;
-  static constexpr int TW = 2;
-  static constexpr int SPAN = (TW - 1) * X::ADV + X::SHMAX + X::L;
-  static constexpr int WSC = SR * SPAN;
-  static constexpr int ROWS = SR * (X::SHMAX + X::L);
-  static constexpr int CCP = CC + 1;
-  static constexpr int HCC = CC;
-  static constexpr int XS = ROWS * WSC * CCP;
-  static constexpr int HS = X::PA * WSC * HCC;
-  static constexpr size_t SMEM = (size_t)(XS + HS) * sizeof(float);
+  static constexpr int TW = 2;                                  // tiles per block along w
+  static constexpr int SPAN = (TW - 1) * X::ADV + X::SHMAX + X::L;  // phase-image columns
+  static constexpr int WSC = SR * SPAN;                         // raw window columns
+  static constexpr int ROWS = SR * (X::SHMAX + X::L);           // raw window rows
+  static constexpr int CSTR = WSC | 1;                          // odd channel stride in Hs
+  static constexpr int NPAIR = CC * SR * SR / 2;                // ce pairs per block
+  static constexpr int HS = X::NPH * SR * X::PA * CC * CSTR;    // floats
+  static constexpr size_t SMEM = (size_t)HS * sizeof(float);
+  static constexpr int THREADS = 256;
 };
 
-template <int MO, int RO, int MI, int SR, typename XT, bool BF>
-__global__ void __launch_bounds__(256) input_transform_kernel(const XT* __restrict__ x, void* __restrict__ Vout,
-                                                              Geometry g) {
+// Outer level of the w-pass for both channels of a pair, one inner point p_i
+// at a time (its l_o outputs share subexpressions), straight into V: points
+// p = p_o * l_i + p_i, so the hi / lo pointers walk p_o with stride l_i points
+// and p_i with stride one point.
+template <int MO, int RO, int MI, bool BF>
+__device__ __forceinline__ void store_row(const float (*za)[Ax<MO, RO, MI>::LI], const float (*zb)[Ax<MO, RO, MI>::LI],
+                                          char* hp, char* lp, long long stride_bytes) {
   using X = Ax<MO, RO, MI>;
-  using C = InCfg<MO, RO, MI, SR>;
-  constexpr int SHIFT[3] = {X::A.shift[0], X::A.shift[1], X::A.shift[2]};
-  extern __shared__ __align__(16) float smem[];
-  float* Xs = smem;
-  float* Hs = smem + C::XS;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wgroups = (g.tiles_w + C::TW - 1) / C::TW;
+#pragma unroll
+  for (int pi = 0; pi < X::LI; ++pi) {
+    float oa[X::LO], ob[X::LO];
+    in_axis_outer_col<MO, RO, MI>(za, pi, oa);
+    in_axis_outer_col<MO, RO, MI>(zb, pi, ob);
+    char* h = hp;
+    char* l = lp;
+#pragma unroll
+    for (int po = 0; po < X::LO; ++po) {
+      if constexpr (BF) {
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(oa[po], ob[po]);
+        const float2 hf = __bfloat1622float2(hi);
+        *reinterpret_cast<__nv_bfloat162*>(h) = hi;
+        *reinterpret_cast<__nv_bfloat162*>(l) = __floats2bfloat162_rn(oa[po] - hf.x, ob[po] - hf.y);
+      } else {
+        *reinterpret_cast<float2*>(h) = make_float2(oa[po], ob[po]);
+      }
+      long long sb = stride_bytes * X::LI;
+      asm volatile("" : "+l"(sb));  // incremental pointer walk (no hoisted per-point offsets)
+      h += sb;
+      if constexpr (BF) l += sb;
+    }
+    long long sb = stride_bytes;
+    asm volatile("" : "+l"(sb));
+    hp += sb;
+    if constexpr (BF) lp += sb;
+  }
+}
+
+template <int MO, int RO, int MI, int SR, int CC, typename XT, bool BF>
+__global__ void __launch_bounds__(256, 2) input_transform_kernel(const XT* __restrict__ x, void* __restrict__ Vout,
+                                                                 Geometry g, int cgroups, int wgroups) {
+  using X = Ax<MO, RO, MI>;
+  using C = InCfg<MO, RO, MI, SR, CC>;
+  constexpr int PA = X::PA, L = X::L, NPH = X::NPH;
+  constexpr int SH1 = X::A.shift[1 < X::A.nph ? 1 : 0];
+  extern __shared__ __align__(16) float Hs[];
+  const int tid = threadIdx.x;
+
   int b = blockIdx.x;
+  const int cg = b % cgroups;
+  b /= cgroups;
   const int wg = b % wgroups;
   b /= wgroups;
   const int ah = b % g.tiles_h;
   const int n = b / g.tiles_h;
-  const int cin0 = blockIdx.y * C::CC;
+  const int cin0 = cg * CC;
   const int aw0 = wg * C::TW;
   const int row0 = SR * (ah * X::ADV) + g.off[0];
   const int col0 = SR * (aw0 * X::ADV) + g.off[0];
 
-  // stage the input region (coalesced along w, zero outside = padding)
-  for (int idx = tid; idx < C::CC * C::ROWS * C::WSC; idx += blockDim.x) {
-    const int c = idx % C::WSC;
-    const int r = (idx / C::WSC) % C::ROWS;
-    const int cc = idx / (C::WSC * C::ROWS);
-    const int gr = row0 + r, gc = col0 + c, ci = cin0 + cc;
-    float v = 0.f;
-    if (ci < g.Cin && gr >= 0 && gr < g.H && gc >= 0 && gc < g.W)
-      v = to_f(x[(((long long)n * g.Cin + ci) * g.H + gr) * g.W + gc]);
-    Xs[(r * C::WSC + c) * C::CCP + cc] = v;
-  }
-
-  const long long plane = (long long)g.P * g.T_pad * g.cin_pad;
+  // ---------------- pass 1: columns along h (straight from x) ----------------
+#pragma unroll 1
+  for (int task = tid; task < CC * C::WSC; task += C::THREADS) {
+    const int col = task % C::WSC, c = task / C::WSC;
+    const int ci = cin0 + c, gc = col0 + col;
+    const bool cok = ci < g.Cin && gc >= 0 && gc < g.W;
+    const XT* src = x + (((long long)n * g.Cin + (cok ? ci : 0)) * g.H) * g.W + (cok ? gc : 0);
+    float xr[C::ROWS];
+    const XT* rp = src + (long long)row0 * g.W;
 #pragma unroll
-  for (int ph = 0; ph < X::NPH; ++ph) {
+    for (int r = 0; r < C::ROWS; ++r) {
+      const int gr = row0 + r;
+      xr[r] = (cok && gr >= 0 && gr < g.H) ? to_f(*rp) : 0.f;
+      long long w = g.W;
+      asm volatile("" : "+l"(w));
+      rp += w;
+    }
 #pragma unroll
-    for (int p = 0; p < SR; ++p) {
-      __syncthreads();
-      // pass 1: columns along h
-      for (int task = tid; task < C::CC * C::WSC; task += blockDim.x) {
-        const int cc = task % C::CC, col = task / C::CC;
-        float xin[X::L], hv[X::PA];
+    for (int ph = 0; ph < NPH; ++ph) {
+      const int sh = ph == 0 ? 0 : SH1;
 #pragma unroll
-        for (int r = 0; r < X::L; ++r)
-          xin[r] = Xs[((SR * (SHIFT[ph] + r) + p) * C::WSC + col) * C::CCP + cc];
+      for (int p = 0; p < SR; ++p) {
+        float xin[L], hv[PA];
+#pragma unroll
+        for (int r = 0; r < L; ++r) xin[r] = xr[SR * (sh + r) + p];
         in_axis<MO, RO, MI>(xin, hv);
+        float* dst = Hs + ((ph * SR + p) * PA * CC + c) * C::CSTR + col;
 #pragma unroll
-        for (int q = 0; q < X::PA; ++q) Hs[(q * C::WSC + col) * C::HCC + cc] = hv[q];
-      }
-      __syncthreads();
-      // pass 2: rows along w, store V
-      constexpr int NTASK = SR * C::CC * C::TW * X::PA;  // multiple of 32
-#pragma unroll
-      for (int pw = 0; pw < X::NPH; ++pw) {
-        for (int base = warp * 32; base < NTASK; base += blockDim.x) {
-          const int task = base + lane;
-          const int q = task % SR;
-          int rest = task / SR;
-          const int cc = rest % C::CC;
-          rest /= C::CC;
-          const int tile = rest % C::TW;
-          const int p_h = rest / C::TW;
-          const int aw = aw0 + tile;
-          const int ci = cin0 + cc;
-          const int ce = (SR == 1) ? ci : ci * 4 + p * 2 + q;
-          const bool valid = (aw < g.tiles_w) && (ce < g.cin_pad);
-          float hin[X::L], vv[X::PA];
-#pragma unroll
-          for (int c = 0; c < X::L; ++c)
-            hin[c] = Hs[(p_h * C::WSC + SR * (tile * X::ADV + SHIFT[pw] + c) + q) * C::HCC + cc];
-          in_axis<MO, RO, MI>(hin, vv);
-          const long long t = ((((long long)n * g.tiles_h + ah) * g.tiles_w + aw) * X::NPH + ph) * X::NPH + pw;
-#pragma unroll
-          for (int p_w = 0; p_w < X::PA; ++p_w) {
-            const long long o = ((long long)(p_h * X::PA + p_w) * g.T_pad + t) * g.cin_pad + ce;
-            if (BF) {
-              const float v = vv[p_w];
-              const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-              const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
-              const unsigned mine = (unsigned)__bfloat16_as_ushort(hi) | ((unsigned)__bfloat16_as_ushort(lo) << 16);
-              const unsigned other = __shfl_xor_sync(0xffffffffu, mine, 1);
-              if (valid) {
-                __nv_bfloat16* V = reinterpret_cast<__nv_bfloat16*>(Vout);
-                if ((lane & 1) == 0) {
-                  *reinterpret_cast<unsigned*>(V + o) = (mine & 0xffffu) | (other << 16);
-                } else {
-                  *reinterpret_cast<unsigned*>(V + plane + o - 1) = (other >> 16) | (mine & 0xffff0000u);
-                }
-              }
-            } else if (valid) {
-              reinterpret_cast<float*>(Vout)[o] = vv[p_w];
-            }
-          }
-        }
+        for (int q = 0; q < PA; ++q) dst[q * CC * C::CSTR] = hv[q];
       }
     }
   }
+  __syncthreads();
+
+  // ---------------- pass 2: rows along w, split, store V ----------------
+  const long long pstride = (long long)g.T_pad * g.cin_pad;  // elements between consecutive points
+  const long long plane = (long long)g.P * pstride;          // hi -> lo plane (bf16 elements)
+  constexpr int NTASK = NPH * NPH * SR * PA * C::TW * (CC * SR / 2);
+#pragma unroll 1
+  for (int task = tid; task < NTASK; task += C::THREADS) {
+    int r = task;
+    const int pr = r % (CC * SR / 2);  // pair within (row phase p): stride 1 channel pair, stride 2 channel
+    r /= (CC * SR / 2);
+    const int tile = r % C::TW;
+    r /= C::TW;
+    const int p_h = r % PA;
+    r /= PA;
+    const int p = r % SR;
+    r /= SR;
+    const int pw = r % NPH;
+    const int phh = r / NPH;
+    const int aw = aw0 + tile;
+    int c0, c1, q0, q1, ce;
+    if (SR == 1) {
+      c0 = 2 * pr; c1 = c0 + 1; q0 = q1 = 0;
+      ce = cin0 + c0;
+    } else {
+      c0 = c1 = pr; q0 = 0; q1 = 1;
+      ce = (cin0 + pr) * 4 + p * 2;
+    }
+    const float* h0 = Hs + (((phh * SR + p) * PA + p_h) * CC + c0) * C::CSTR;
+    const float* h1 = Hs + (((phh * SR + p) * PA + p_h) * CC + c1) * C::CSTR;
+    const int cb = tile * X::ADV + (pw == 0 ? 0 : SH1);
+    if (aw >= g.tiles_w || ce >= g.cin_pad) continue;
+    float za[X::LO][X::LI], zb[X::LO][X::LI];
+    {
+      float a[L], bb[L];
+#pragma unroll
+      for (int k = 0; k < L; ++k) {
+        a[k] = h0[SR * (cb + k) + q0];
+        bb[k] = h1[SR * (cb + k) + q1];
+      }
+      in_axis_inner<MO, RO, MI>(a, za);
+      in_axis_inner<MO, RO, MI>(bb, zb);
+    }
+    const long long t = ((((long long)n * g.tiles_h + ah) * g.tiles_w + aw) * NPH + phh) * NPH + pw;
+    const long long o = ((long long)(p_h * PA) * g.T_pad + t) * g.cin_pad + ce;
+    constexpr int ES = BF ? 2 : 4;
+    char* hp = reinterpret_cast<char*>(Vout) + o * ES;
+    store_row<MO, RO, MI, BF>(za, zb, hp, hp + plane * ES, pstride * ES);
+  }
 }
 
-}  // namespace nw
-
-namespace nw {
-
-template <int MO, int RO, int MI, int SR, typename XT, bool BF>
+template <int MO, int RO, int MI, int SR, int CC, typename XT, bool BF>
 static nw_status_t input_launch(const Geometry& g, const void* x, void* V, cudaStream_t s) {
-  using C = InCfg<MO, RO, MI, SR>;
-  auto kern = input_transform_kernel<MO, RO, MI, SR, XT, BF>;
+  using C = InCfg<MO, RO, MI, SR, CC>;
+  auto kern = input_transform_kernel<MO, RO, MI, SR, CC, XT, BF>;
   static bool attr_done = false;  // per instantiation
   if (!attr_done) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
@@ -145,15 +189,25 @@ static nw_status_t input_launch(const Geometry& g, const void* x, void* V, cudaS
     attr_done = true;
   }
   const int wgroups = (g.tiles_w + C::TW - 1) / C::TW;
-  const long long gx = (long long)g.N * g.tiles_h * wgroups;
   const int cin_src = (SR == 1) ? g.cin_pad : g.cin_pad / 4;
-  dim3 grid((unsigned)gx, (unsigned)((cin_src + C::CC - 1) / C::CC));
+  const int cgroups = (cin_src + CC - 1) / CC;
+  const long long nb = (long long)g.N * g.tiles_h * wgroups * cgroups;
+  if (nb >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
   LaunchScope scope_("input_transform", s);
-  kern<<<grid, 256, C::SMEM, s>>>(static_cast<const XT*>(x), V, g);
+  kern<<<(unsigned)nb, C::THREADS, C::SMEM, s>>>(static_cast<const XT*>(x), V, g, cgroups, wgroups);
   return check_launch();
 }
 
-// Instantiated per axis combo in input_<mo><ro><mi>.cu.  Stride-2 phases and
+// Channel-group width: 32 source channels (64-byte V segments per plane) when
+// the layer has them, else 16; stride 2 folds 4 phases per channel, so 8.
+template <int MO, int RO, int MI, int SR, typename XT, bool BF>
+static nw_status_t input_pick(const Geometry& g, const void* x, void* V, cudaStream_t s) {
+  if (SR == 2) return input_launch<MO, RO, MI, SR, 8, XT, BF>(g, x, V, s);
+  if (Ax<MO, RO, MI>::NPH == 1 && g.cin_pad >= 32) return input_launch<MO, RO, MI, SR, 32, XT, BF>(g, x, V, s);
+  return input_launch<MO, RO, MI, SR, 16, XT, BF>(g, x, V, s);
+}
+
+// Instantiated per axis combo in xform_<mo><ro><mi>.cu.  Stride-2 phases and
 // bf16 storage are built for the combos the BASELINE configs use.
 template <int MO, int RO, int MI>
 nw_status_t input_impl(const nw_plan_st* p, const Geometry& g, const void* x, void* V, cudaStream_t s) {
@@ -164,20 +218,20 @@ nw_status_t input_impl(const nw_plan_st* p, const Geometry& g, const void* x, vo
   if (g.SR == 1) {
     if (xb) {
       if constexpr (kBf16In) {
-        return bf ? input_launch<MO, RO, MI, 1, __nv_bfloat16, true>(g, x, V, s)
-                  : input_launch<MO, RO, MI, 1, __nv_bfloat16, false>(g, x, V, s);
+        return bf ? input_pick<MO, RO, MI, 1, __nv_bfloat16, true>(g, x, V, s)
+                  : input_pick<MO, RO, MI, 1, __nv_bfloat16, false>(g, x, V, s);
       }
       return NW_ERR_UNSUPPORTED;
     }
-    return bf ? input_launch<MO, RO, MI, 1, float, true>(g, x, V, s)
-              : input_launch<MO, RO, MI, 1, float, false>(g, x, V, s);
+    return bf ? input_pick<MO, RO, MI, 1, float, true>(g, x, V, s)
+              : input_pick<MO, RO, MI, 1, float, false>(g, x, V, s);
   }
   if constexpr (kFull) {
     if (xb)
-      return bf ? input_launch<MO, RO, MI, 2, __nv_bfloat16, true>(g, x, V, s)
-                : input_launch<MO, RO, MI, 2, __nv_bfloat16, false>(g, x, V, s);
-    return bf ? input_launch<MO, RO, MI, 2, float, true>(g, x, V, s)
-              : input_launch<MO, RO, MI, 2, float, false>(g, x, V, s);
+      return bf ? input_pick<MO, RO, MI, 2, __nv_bfloat16, true>(g, x, V, s)
+                : input_pick<MO, RO, MI, 2, __nv_bfloat16, false>(g, x, V, s);
+    return bf ? input_pick<MO, RO, MI, 2, float, true>(g, x, V, s)
+              : input_pick<MO, RO, MI, 2, float, false>(g, x, V, s);
   }
   return NW_ERR_UNSUPPORTED;
 }

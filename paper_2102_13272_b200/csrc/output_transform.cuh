@@ -1,132 +1,265 @@
 // output_transform.cuh -- G4: nested output transform fused with the store.
 // Instantiated per axis combo in xform_*.cu.
 //
-// M layout [P][cout_pad][T_pad] (fp32): one warp owns 32 consecutive slices of one
-// output channel, so every load of M is a 128-byte coalesced row.  Each thread
-// keeps the 9x9 (M_a x M_a) output tile of its slice in registers: for each
-// point row p_h it applies A^T_hat along w (factored, 25 -> 9) and accumulates
-// A^T_hat[q_h][p_h] times that row into the tile (composite along h, zero
-// coefficients skipped at compile time).  The tile then goes through a per-warp
-// shared-memory stage so the stores walk whole output rows across the 32 slices
-// (adjacent tiles are adjacent in w), applying the keep mask (redundant terms /
-// coverage phases), the crop, the transposed-conv depth-to-space, PReLU and the
-// dtype cast.
+// Y = A^T_hat M A_hat per (slice, output channel), then keep mask (redundant
+// terms / coverage phases), crop of ragged tiles, depth-to-space of the
+// transposed-conv output phases, PReLU and the dtype cast, stored NCHW.
+//
+// M layout [P][cout_pad][T_pad] fp32.  Persistent kernel, one CTA per SM:
+//   warp CO (one elected lane)  TMA producer: one box {32 slices, CO channels,
+//                               P_a points} = one point row p_h per ring stage
+//   warps 0..CO-1               consumers, warp = output channel, lane = slice
+// A unit is (32 consecutive slices, CO channels); its P_a point rows stream
+// through an NST-deep ring, so HBM reads stay in flight while the consumers
+// compute.  Per point row a consumer applies A^T_hat along w (factored, 25 -> 9,
+// compile-time coefficients), accumulates the inner-level A_i^T along h into
+// u[m_i][M_a] and, once per outer point p_o, folds u into the output tile with
+// A_o^T[t][p_o] (the outer loop is not unrolled, which keeps the kernel inside
+// the instruction cache).  The finished tile goes through a per-warp shared
+// stage so the stores walk output rows across the 32 slices.
 #pragma once
+#include "ptx.cuh"
 #include "transforms.cuh"
 
 namespace nw {
 
-struct AtHatF {
-  float a[kMaxMa][kMaxPa];
-};
-template <int MO, int RO, int MI>
-__host__ __device__ constexpr AtHatF make_athat() {
-  AtHatF T{};
-  NestedAxis A = make_axis(MO, RO, MI);
-  for (int q = 0; q < A.Ma; ++q)
-    for (int p = 0; p < A.Pa; ++p) T.a[q][p] = float(rdouble(at_hat(A, q, p)));
-  return T;
-}
-
 template <int MO, int RO, int MI>
 struct OutCfg {
   using X = Ax<MO, RO, MI>;
-  static constexpr int WARPS = 8;
-  static constexpr int STAGE = 32 * X::MA * X::MA + 1;  // floats per warp (odd stride per slice)
-  static constexpr size_t SMEM = (size_t)WARPS * STAGE * sizeof(float);
+  static constexpr int CO = 8;   // output channels per unit (consumer warps)
+  static constexpr int TS = 32;  // slices per unit (lanes)
+  static constexpr int NST = 4;  // ring depth (point rows)
+  static constexpr int STAGE = X::PA * CO * TS;     // floats per ring stage
+  static constexpr int YST = TS * X::MA * X::MA + 1; // floats per warp output stage
+  static constexpr int THREADS = (CO + 1) * 32;
+  static constexpr size_t RING_BYTES = (size_t)NST * STAGE * 4;
+  static constexpr size_t YST_BYTES = (size_t)CO * YST * 4;
+  static constexpr size_t INFO_BYTES = (size_t)CO * TS * 16;
+  static constexpr size_t SMEM = 128 + RING_BYTES + YST_BYTES + INFO_BYTES + 2 * NST * 8;
 };
 
+// out_pos / keep as compile-time tables
+template <int MO, int RO, int MI>
+struct OutTables {
+  int pos[kMaxMa];
+  unsigned keep[3];  // per coverage phase, bit q
+  int shift[3];      // coverage-phase shift
+};
+template <int MO, int RO, int MI>
+__host__ __device__ constexpr OutTables<MO, RO, MI> make_out_tables() {
+  OutTables<MO, RO, MI> T{};
+  NestedAxis A = make_axis(MO, RO, MI);
+  for (int q = 0; q < A.Ma; ++q) T.pos[q] = out_pos(A, q);
+  for (int ph = 0; ph < 3; ++ph) {
+    unsigned m = 0;
+    if (ph < A.nph)
+      for (int q = 0; q < A.Ma; ++q)
+        if (keep(A, ph, q)) m |= 1u << q;
+    T.keep[ph] = m;
+    T.shift[ph] = A.shift[ph];
+  }
+  return T;
+}
+
+// select v[i] for a runtime i from a compile-time row (a chain of selects)
+template <int N>
+__device__ __forceinline__ float csel(const float (&v)[kMaxL], int i) {
+  float r = v[0];
+#pragma unroll
+  for (int k = 1; k < N; ++k) r = (i == k) ? v[k] : r;
+  return r;
+}
+
 template <int MO, int RO, int MI, typename YT>
-__global__ void __launch_bounds__(256, 2) output_transform_kernel(const float* __restrict__ M, YT* __restrict__ y,
-                                                                  Geometry g, const float* __restrict__ slopes) {
+__global__ void __launch_bounds__(OutCfg<MO, RO, MI>::THREADS, 1)
+    output_transform_kernel(const __grid_constant__ CUtensorMap mapM, YT* __restrict__ y, Geometry g,
+                            const float* __restrict__ slopes, int nunits, int ngroups) {
   using X = Ax<MO, RO, MI>;
   using C = OutCfg<MO, RO, MI>;
-  constexpr NestedAxis A = make_axis(MO, RO, MI);
-  constexpr AtHatF AT = make_athat<MO, RO, MI>();
-  constexpr int MA = X::MA, PA = X::PA, NPH = X::NPH;
-  extern __shared__ __align__(16) float smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float* stage = smem + warp * C::STAGE;
+  constexpr AxisF F = axis_f(MO, RO, MI);
+  constexpr OutTables<MO, RO, MI> OT = make_out_tables<MO, RO, MI>();
+  constexpr int MA = X::MA, PA = X::PA, LO = X::LO, LI = X::LI, NPH = X::NPH;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  // 128-byte aligned base derived from the shared array itself (keeps loads in the shared window: LDS, not LD)
+  uint8_t* base = smem_raw + ((128u - (ptx::smem_u32(smem_raw) & 127u)) & 127u);
+  float* ring = reinterpret_cast<float*>(base);
+  float* ystage = reinterpret_cast<float*>(base + C::RING_BYTES);
+  long long* sinfo = reinterpret_cast<long long*>(base + C::RING_BYTES + C::YST_BYTES);  // [CO][TS][2]
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + C::RING_BYTES + C::YST_BYTES + C::INFO_BYTES);
+  uint64_t* empty = full + C::NST;
 
-  const long long t0 = (long long)blockIdx.x * 32;
-  const int coe = blockIdx.y * C::WARPS + warp;
-  if (coe >= g.cout_e) return;
-  const long long t = t0 + lane;
-  const bool valid = t < g.T;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NST; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&empty[i]), C::CO);
+    }
+    ptx::mbar_init_fence();
+  }
+  __syncthreads();
 
-  float Y[MA][MA];
-#pragma unroll
-  for (int i = 0; i < MA; ++i)
-#pragma unroll
-    for (int j = 0; j < MA; ++j) Y[i][j] = 0.f;
-
-  const long long pstride = (long long)g.cout_pad * g.T_pad;   // between consecutive points
-  const float* src = M + (long long)coe * g.T_pad + (valid ? t : 0);
-#pragma unroll
-  for (int p_h = 0; p_h < PA; ++p_h) {
-    float mv[PA], qv[MA];
-#pragma unroll
-    for (int p_w = 0; p_w < PA; ++p_w) mv[p_w] = __ldg(src + (long long)(p_h * PA + p_w) * pstride);
-    out_axis<MO, RO, MI>(mv, qv);
-#pragma unroll
-    for (int q_h = 0; q_h < MA; ++q_h) {
-      if (AT.a[q_h][p_h] != 0.f) {
-#pragma unroll
-        for (int q_w = 0; q_w < MA; ++q_w) Y[q_h][q_w] = fmaf(AT.a[q_h][p_h], qv[q_w], Y[q_h][q_w]);
+  if (warp == C::CO) {
+    // ------------------------------ TMA producer ------------------------------
+    if (lane == 0) {
+      ptx::tma_prefetch(&mapM);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int t0 = (u / ngroups) * C::TS, co0 = (u % ngroups) * C::CO;
+        for (int r = 0; r < PA; ++r) {
+          ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
+          const uint32_t fb = ptx::smem_u32(&full[st]);
+          ptx::mbar_expect_tx(fb, C::STAGE * 4);
+          ptx::tma_load_3d(ptx::smem_u32(ring + st * C::STAGE), &mapM, fb, t0, co0, r * PA);
+          if (++st == C::NST) { st = 0; ph ^= 1; }
+        }
       }
     }
+    return;
   }
 
-  // stage the tile: stage[lane * MA*MA + q_h*MA + q_w]
-#pragma unroll
-  for (int q_h = 0; q_h < MA; ++q_h)
-#pragma unroll
-    for (int q_w = 0; q_w < MA; ++q_w) stage[lane * (MA * MA) + q_h * MA + q_w] = Y[q_h][q_w];
-  __syncwarp();
+  // -------------------------------- consumers ---------------------------------
+  float* yst = ystage + warp * C::YST;
+  long long* info = sinfo + warp * (C::TS * 2);
+  const long long HoWo = (long long)g.Ho * g.Wo;
+  const int rowstride = (g.mode == 2) ? 2 * g.Wo : g.Wo;
+  const int colstride = (g.mode == 2) ? 2 : 1;
+  int st = 0;
+  uint32_t ph = 0;
+  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const long long t0 = (long long)(u / ngroups) * C::TS;
+    const int coe = (u % ngroups) * C::CO + warp;
 
-  // store: index = (q_h, slice, q_w) so consecutive lanes walk one output row across slices
-  int c = coe, fo_h = 0, fo_w = 0;
-  if (g.mode == 2) {
-    const int f = coe / g.Cout;
-    c = coe % g.Cout;
-    fo_h = f / 2;
-    fo_w = f % 2;
-  }
-  const float slope = slopes ? slopes[c] : 0.f;
-  const long long nslices = g.T - t0 < 32 ? g.T - t0 : 32;
-  for (int idx = lane; idx < 32 * MA * MA; idx += 32) {
-    const int q_w = idx % MA;
-    const int s = (idx / MA) % 32;
-    const int q_h = idx / (MA * 32);
-    if (s >= nslices) continue;
-    long long ts = t0 + s;
-    const int phw = (int)(ts % NPH);
-    ts /= NPH;
-    const int phh = (int)(ts % NPH);
-    ts /= NPH;
-    const int aw = (int)(ts % g.tiles_w);
-    ts /= g.tiles_w;
-    const int ah = (int)(ts % g.tiles_h);
-    const int n = (int)(ts / g.tiles_h);
-    if (!keep(A, phh, q_h) || !keep(A, phw, q_w)) continue;
-    const int gi = ah * X::ADV + A.shift[phh] + out_pos(A, q_h);
-    const int gj = aw * X::ADV + A.shift[phw] + out_pos(A, q_w);
-    if (gi >= g.Hq || gj >= g.Wq) continue;
-    int Yr = gi, Xc = gj;
-    if (g.mode == 2) {
-      Yr = 2 * gi + fo_h;
-      Xc = 2 * gj + fo_w;
-      if (Yr >= g.Ho || Xc >= g.Wo) continue;
+    float Y[MA][MA];
+#pragma unroll
+    for (int i = 0; i < MA; ++i)
+#pragma unroll
+      for (int j = 0; j < MA; ++j) Y[i][j] = 0.f;
+
+#pragma unroll 1
+    for (int p_o = 0; p_o < LO; ++p_o) {
+      float uacc[MI][MA];
+#pragma unroll
+      for (int s = 0; s < MI; ++s)
+#pragma unroll
+        for (int j = 0; j < MA; ++j) uacc[s][j] = 0.f;
+#pragma unroll
+      for (int p_i = 0; p_i < LI; ++p_i) {
+        ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
+        const float* src = ring + st * C::STAGE + warp * C::TS + lane;
+        float mv[PA], qv[MA];
+#pragma unroll
+        for (int p_w = 0; p_w < PA; ++p_w) mv[p_w] = src[p_w * (C::CO * C::TS)];
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[st]));
+        if (++st == C::NST) { st = 0; ph ^= 1; }
+        out_axis<MO, RO, MI>(mv, qv);
+#pragma unroll
+        for (int s = 0; s < MI; ++s) {
+          const float a = F.AiT[s][p_i];
+          if (a == 1.f) {
+#pragma unroll
+            for (int j = 0; j < MA; ++j) uacc[s][j] += qv[j];
+          } else if (a == -1.f) {
+#pragma unroll
+            for (int j = 0; j < MA; ++j) uacc[s][j] -= qv[j];
+          } else if (a != 0.f) {
+#pragma unroll
+            for (int j = 0; j < MA; ++j) uacc[s][j] = fmaf(a, qv[j], uacc[s][j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < MO; ++t) {
+        const float c = csel<LO>(F.AoT[t], p_o);
+#pragma unroll
+        for (int s = 0; s < MI; ++s)
+#pragma unroll
+          for (int j = 0; j < MA; ++j) Y[t * MI + s][j] = fmaf(c, uacc[s][j], Y[t * MI + s][j]);
+      }
     }
-    float v = stage[s * (MA * MA) + q_h * MA + q_w];
-    if (slopes) v = v >= 0.f ? v : slope * v;
-    y[(((long long)n * g.Cout + c) * g.Ho + Yr) * g.Wo + Xc] = from_f<YT>(v);
+
+    // ---- epilogue: per-slice store geometry (lane = slice), tile -> stage ----
+    {
+      const long long ts_ = t0 + lane;
+      long long b = -1;
+      int lim = 0;
+      if (ts_ < g.T && coe < g.cout_e) {
+        long long tt = ts_;
+        const int phw = (int)(tt % NPH);
+        tt /= NPH;
+        const int phh = (int)(tt % NPH);
+        tt /= NPH;
+        const int aw = (int)(tt % g.tiles_w);
+        tt /= g.tiles_w;
+        const int ah = (int)(tt % g.tiles_h);
+        const int n = (int)(tt / g.tiles_h);
+        int c = coe, fo_h = 0, fo_w = 0;
+        if (g.mode == 2) {
+          const int f = coe / g.Cout;
+          c = coe % g.Cout;
+          fo_h = f / 2;
+          fo_w = f % 2;
+        }
+        const int gi0 = ah * X::ADV + (phh == 0 ? OT.shift[0] : phh == 1 ? OT.shift[1] : OT.shift[2]);   // stride-1 grid row of q position 0
+        const int gj0 = aw * X::ADV + (phw == 0 ? OT.shift[0] : phw == 1 ? OT.shift[1] : OT.shift[2]);
+        int limh, limw;  // positions p with gi0 + p inside the output
+        if (g.mode == 2) {
+          limh = (g.Ho - fo_h + 1) / 2 - gi0;
+          limw = (g.Wo - fo_w + 1) / 2 - gj0;
+          b = ((long long)n * g.Cout + c) * HoWo + (long long)(2 * gi0 + fo_h) * g.Wo + (2 * gj0 + fo_w);
+        } else {
+          limh = g.Hq - gi0;
+          limw = g.Wq - gj0;
+          b = ((long long)n * g.Cout + c) * HoWo + (long long)gi0 * g.Wo + gj0;
+        }
+        limh = limh < 0 ? 0 : (limh > 255 ? 255 : limh);
+        limw = limw < 0 ? 0 : (limw > 255 ? 255 : limw);
+        lim = limh | (limw << 8) | (phh << 16) | (phw << 18);
+      }
+      info[lane * 2] = b;
+      info[lane * 2 + 1] = lim;
+    }
+#pragma unroll
+    for (int i = 0; i < MA; ++i)
+#pragma unroll
+      for (int j = 0; j < MA; ++j) yst[lane * (MA * MA) + i * MA + j] = Y[i][j];
+    __syncwarp();
+    const float slope = (slopes && coe < g.cout_e) ? slopes[g.mode == 2 ? coe % g.Cout : coe] : 0.f;
+#pragma unroll 1
+    for (int jj = 0; jj < MA; ++jj) {
+      const int e = lane + 32 * jj;  // (slice s, column q_w) pairs, q_w fastest
+      const int s = e / MA, q_w = e - s * MA;
+      const uint32_t ia = ptx::smem_u32(info) + (uint32_t)s * 16u;
+      const long long b = ptx::lds_s64(ia);
+      const int lim = (int)ptx::lds_s64(ia + 8);
+      const uint32_t ya = ptx::smem_u32(yst) + (uint32_t)(s * (MA * MA) + q_w) * 4u;
+      const int limh = lim & 255, limw = (lim >> 8) & 255;
+      const int khi = (lim >> 16) & 3, kwi = (lim >> 18) & 3;
+      const unsigned kh = khi == 0 ? OT.keep[0] : khi == 1 ? OT.keep[1] : OT.keep[2];
+      const unsigned kw = kwi == 0 ? OT.keep[0] : kwi == 1 ? OT.keep[1] : OT.keep[2];
+      int pw = 0;
+#pragma unroll
+      for (int q = 0; q < MA; ++q) pw = (q_w == q) ? OT.pos[q] : pw;
+      const bool okw = b >= 0 && ((kw >> q_w) & 1u) && pw < limw;
+      YT* dst = y + (b < 0 ? 0 : b) + (long long)pw * colstride;
+#pragma unroll
+      for (int q_h = 0; q_h < MA; ++q_h) {
+        if (okw && ((kh >> q_h) & 1u) && OT.pos[q_h] < limh) {
+          float v = ptx::lds_f32(ya + q_h * MA * 4);
+          if (slopes) v = v >= 0.f ? v : slope * v;
+          dst[(long long)OT.pos[q_h] * rowstride] = from_f<YT>(v);
+        }
+      }
+    }
+    __syncwarp();
   }
 }
 
 template <int MO, int RO, int MI, typename YT>
 static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const float* M, void* y, cudaStream_t s) {
   using C = OutCfg<MO, RO, MI>;
+  using X = Ax<MO, RO, MI>;
   auto kern = output_transform_kernel<MO, RO, MI, YT>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -134,9 +267,21 @@ static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const f
       return NW_ERR_CUDA;
     attr_done = true;
   }
-  dim3 grid((unsigned)((g.T + 31) / 32), (unsigned)((g.cout_e + C::WARPS - 1) / C::WARPS));
+  alignas(64) CUtensorMap map;
+  const uint64_t dims[3] = {(uint64_t)g.T_pad, (uint64_t)g.cout_pad, (uint64_t)g.P};
+  const uint64_t strides[2] = {(uint64_t)g.T_pad * 4, (uint64_t)g.T_pad * g.cout_pad * 4};
+  const uint32_t box[3] = {(uint32_t)C::TS, (uint32_t)C::CO, (uint32_t)X::PA};
+  if (!encode_tmap(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, M, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return NW_ERR_CUDA;
+  const int ngroups = g.cout_pad / C::CO;
+  const long long tchunks = (g.T + C::TS - 1) / C::TS;
+  const long long nunits = tchunks * ngroups;
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)(nunits < sms ? nunits : sms);
   LaunchScope scope_("output_transform", s);
-  kern<<<grid, 32 * C::WARPS, C::SMEM, s>>>(M, static_cast<YT*>(y), g, p->prelu ? p->slopes : nullptr);
+  kern<<<grid, C::THREADS, C::SMEM, s>>>(map, static_cast<YT*>(y), g, p->prelu ? p->slopes : nullptr, (int)nunits,
+                                         ngroups);
   return check_launch();
 }
 

@@ -5,8 +5,13 @@
 //   G4 output transform   Y = A^T_hat M A_hat + scatter/keep + store
 // The transforms are compile-time (constexpr Cook-Toom, cooktoom.cuh), applied
 // per axis in the factored two-level form (B_o^T (x) B_i^T: inner F(m_i,3) on each
-// reordered column, then outer F(m_o,r_o) across columns) so zero entries and
-// +-1 coefficients vanish from the instruction stream.
+// reordered column, then outer F(m_o,r_o) across columns).  Each level is one
+// 1-D kernel (K1<m,r>::bt / ::at): generic kernels skip zero and +-1 coefficients at
+// compile time; F(3,3) -- the kernel at both levels of the default plan -- has
+// hand-factored forms with shared subexpressions (9 instead of 18 operations
+// for B^T, 7 instead of 11 for A^T).  Float addition is not associative, so the
+// compiler cannot find these factorizations itself; the rounding order differs
+// from the plain matrix product by a few ulp, far inside the accuracy budget.
 #pragma once
 #include <cuda_bf16.h>
 
@@ -22,86 +27,137 @@ struct Ax {
 };
 
 // ---------------------------------------------------------------------------
-// per-axis transforms (factored), float
+// one-level 1-D kernels: out[l] = B^T in[l] (l = m + r - 1), out[m] = A^T in[l]
 // ---------------------------------------------------------------------------
-// x[L] (slice window along one axis) -> v[PA] = B^T_hat x
+template <int M, int R>
+struct K1 {
+  static constexpr int L = M + R - 1;
+  __device__ __forceinline__ static void bt(const float (&x)[L], float (&o)[L]) {
+    constexpr Kernel1D K = make_kernel(M, R);
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      float acc = 0.f;
+      bool first = true;
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        const float c = float(rdouble(K.BT[i][j]));
+        if (c != 0.f) {
+          const float t = (c == 1.f) ? x[j] : (c == -1.f) ? -x[j] : c * x[j];
+          acc = first ? t : ((c == -1.f) ? acc - x[j] : (c == 1.f) ? acc + x[j] : fmaf(c, x[j], acc));
+          first = false;
+        }
+      }
+      o[i] = acc;
+    }
+  }
+  __device__ __forceinline__ static void at(const float (&x)[L], float (&o)[M]) {
+    constexpr Kernel1D K = make_kernel(M, R);
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      float acc = 0.f;
+      bool first = true;
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        const float c = float(rdouble(K.AT[i][j]));
+        if (c != 0.f) {
+          const float t = (c == 1.f) ? x[j] : (c == -1.f) ? -x[j] : c * x[j];
+          acc = first ? t : ((c == -1.f) ? acc - x[j] : (c == 1.f) ? acc + x[j] : fmaf(c, x[j], acc));
+          first = false;
+        }
+      }
+      o[i] = acc;
+    }
+  }
+};
+
+// F(3,3), points {0, 1, -1, 2, inf} (R2):
+//   B^T = [2 -1 -2 1 0; 0 2 1 -1 0; 0 -2 3 -1 0; 0 -1 0 1 0; 0 2 -1 -2 1]
+//   A^T = [1 1 1 1 0; 0 1 -1 2 0; 0 1 1 4 1]
+template <>
+struct K1<3, 3> {
+  static constexpr int L = 5;
+  __device__ __forceinline__ static void bt(const float (&x)[5], float (&o)[5]) {
+    const float a = x[3] - x[1];                         // row 3
+    o[3] = a;
+    o[0] = fmaf(2.f, x[0] - x[2], a);                    // 2x0 - x1 - 2x2 + x3
+    o[1] = (x[1] + x[2]) - a;                            // 2x1 + x2 - x3
+    o[2] = fmaf(2.f, fmaf(-2.f, x[1], x[2]), o[1]);      // -2x1 + 3x2 - x3
+    o[4] = fmaf(-2.f, a, x[4] - x[2]);                   // 2x1 - x2 - 2x3 + x4
+  }
+  __device__ __forceinline__ static void at(const float (&x)[5], float (&o)[3]) {
+    const float s = x[1] + x[2], d = x[1] - x[2];
+    o[0] = (x[0] + x[3]) + s;                            // x0 + x1 + x2 + x3
+    o[1] = fmaf(2.f, x[3], d);                           // x1 - x2 + 2x3
+    o[2] = fmaf(4.f, x[3], s) + x[4];                    // x1 + x2 + 4x3 + x4
+  }
+};
+
+// ---------------------------------------------------------------------------
+// per-axis two-level transforms, float
+// ---------------------------------------------------------------------------
+// inner level on every reordered column: z[j][p_i] = (B_i^T x[3j .. 3j + l_i))[p_i]
+template <int MO, int RO, int MI>
+__device__ __forceinline__ void in_axis_inner(const float* x, float (*z)[Ax<MO, RO, MI>::LI]) {
+  using X = Ax<MO, RO, MI>;
+#pragma unroll
+  for (int j = 0; j < X::LO; ++j) {
+    float col[X::LI], o[X::LI];
+#pragma unroll
+    for (int s = 0; s < X::LI; ++s) col[s] = x[kRi * j + s];
+    K1<MI, kRi>::bt(col, o);
+#pragma unroll
+    for (int s = 0; s < X::LI; ++s) z[j][s] = o[s];
+  }
+}
+// outer level for one inner point p_i: o[p_o] = (B_o^T z[.][p_i])[p_o]
+template <int MO, int RO, int MI>
+__device__ __forceinline__ void in_axis_outer_col(const float (*z)[Ax<MO, RO, MI>::LI], int pi,
+                                                  float (&o)[Ax<MO, RO, MI>::LO]) {
+  using X = Ax<MO, RO, MI>;
+  float c[X::LO];
+#pragma unroll
+  for (int j = 0; j < X::LO; ++j) c[j] = z[j][pi];
+  K1<MO, RO>::bt(c, o);
+}
+
+// x[L] (slice window along one axis) -> v[PA] = B^T_hat x, point p = p_o * l_i + p_i
 template <int MO, int RO, int MI>
 __device__ __forceinline__ void in_axis(const float* x, float* v) {
   using X = Ax<MO, RO, MI>;
-  constexpr AxisF F = axis_f(MO, RO, MI);
   float z[X::LO][X::LI];
+  in_axis_inner<MO, RO, MI>(x, z);
 #pragma unroll
-  for (int j = 0; j < X::LO; ++j)
+  for (int pi = 0; pi < X::LI; ++pi) {
+    float o[X::LO];
+    in_axis_outer_col<MO, RO, MI>(z, pi, o);
 #pragma unroll
-    for (int pi = 0; pi < X::LI; ++pi) {
-      float acc = 0.f;
-      bool first = true;
-#pragma unroll
-      for (int s = 0; s < X::LI; ++s) {
-        if (F.BiT[pi][s] != 0.f) {
-          const float t = F.BiT[pi][s] * x[kRi * j + s];
-          acc = first ? t : acc + t;
-          first = false;
-        }
-      }
-      z[j][pi] = acc;
-    }
-#pragma unroll
-  for (int po = 0; po < X::LO; ++po)
-#pragma unroll
-    for (int pi = 0; pi < X::LI; ++pi) {
-      float acc = 0.f;
-      bool first = true;
-#pragma unroll
-      for (int j = 0; j < X::LO; ++j) {
-        if (F.BoT[po][j] != 0.f) {
-          const float t = F.BoT[po][j] * z[j][pi];
-          acc = first ? t : acc + t;
-          first = false;
-        }
-      }
-      v[po * X::LI + pi] = acc;
-    }
+    for (int po = 0; po < X::LO; ++po) v[po * X::LI + pi] = o[po];
+  }
 }
 
-// m[PA] -> y[MA] = A^T_hat m
+// m[PA] -> y[MA] = A^T_hat m, output q = t * m_i + s
 template <int MO, int RO, int MI>
 __device__ __forceinline__ void out_axis(const float* m, float* y) {
   using X = Ax<MO, RO, MI>;
-  constexpr AxisF F = axis_f(MO, RO, MI);
   float u[X::LO][MI];
 #pragma unroll
-  for (int po = 0; po < X::LO; ++po)
+  for (int po = 0; po < X::LO; ++po) {
+    float col[X::LI], o[MI];
 #pragma unroll
-    for (int s = 0; s < MI; ++s) {
-      float acc = 0.f;
-      bool first = true;
+    for (int pi = 0; pi < X::LI; ++pi) col[pi] = m[po * X::LI + pi];
+    K1<MI, kRi>::at(col, o);
 #pragma unroll
-      for (int pi = 0; pi < X::LI; ++pi) {
-        if (F.AiT[s][pi] != 0.f) {
-          const float t = F.AiT[s][pi] * m[po * X::LI + pi];
-          acc = first ? t : acc + t;
-          first = false;
-        }
-      }
-      u[po][s] = acc;
-    }
+    for (int s = 0; s < MI; ++s) u[po][s] = o[s];
+  }
 #pragma unroll
-  for (int t = 0; t < MO; ++t)
+  for (int s = 0; s < MI; ++s) {
+    float col[X::LO], o[MO];
 #pragma unroll
-    for (int s = 0; s < MI; ++s) {
-      float acc = 0.f;
-      bool first = true;
+    for (int po = 0; po < X::LO; ++po) col[po] = u[po][s];
+    K1<MO, RO>::at(col, o);
 #pragma unroll
-      for (int po = 0; po < X::LO; ++po) {
-        if (F.AoT[t][po] != 0.f) {
-          const float v = F.AoT[t][po] * u[po][s];
-          acc = first ? v : acc + v;
-          first = false;
-        }
-      }
-      y[t * MI + s] = acc;
-    }
+    for (int t = 0; t < MO; ++t) y[t * MI + s] = o[t];
+  }
 }
 
 template <typename T>
