@@ -1,4 +1,5 @@
-// dispatch.cu -- route a plan's (m_o, r_o, m_i) to its compiled transform kernels.
+// dispatch.cu -- route a geometry's axis kernel (m_o, r_o, m_i) to its compiled transform kernels
+// (the plan's nested kernel, or F(1,1) (x) F(3,3) = single-level F(3,3) for the OLA path).
 #include "nw_internal.h"
 
 namespace nw {
@@ -10,11 +11,12 @@ nw_status_t output_impl(const nw_plan_st*, const Geometry&, const float*, void*,
 
 #define NW_DISPATCH_AXIS(p, FN, ...)                                       \
   do {                                                                     \
-    const int mo_ = (p)->m_o, ro_ = (p)->r_o, mi_ = (p)->m_i;              \
+    const int mo_ = g.mo, ro_ = g.ro, mi_ = g.mi;                          \
     if (mo_ == 3 && ro_ == 3 && mi_ == 3) return FN<3, 3, 3>(__VA_ARGS__); \
     if (mo_ == 2 && ro_ == 3 && mi_ == 2) return FN<2, 3, 2>(__VA_ARGS__); \
     if (mo_ == 3 && ro_ == 2 && mi_ == 3) return FN<3, 2, 3>(__VA_ARGS__); \
     if (mo_ == 2 && ro_ == 3 && mi_ == 3) return FN<2, 3, 3>(__VA_ARGS__); \
+    if (mo_ == 1 && ro_ == 1 && mi_ == 3) return FN<1, 1, 3>(__VA_ARGS__); \
     return NW_ERR_UNSUPPORTED;                                             \
   } while (0)
 

@@ -27,10 +27,15 @@ __device__ __forceinline__ double ld_w<__nv_bfloat16>(const __nv_bfloat16* w, lo
 template <typename WT, bool BF>
 __global__ void __launch_bounds__(128) filter_transform_kernel(const WT* __restrict__ w, void* __restrict__ Uout,
                                                                Geometry g, int K, const __grid_constant__ GhatParam G) {
+  // one thread per (output channel coe, filter block b, contraction channel ce);
+  // U layout [P][cout_pad][nsh * cin_pad], K index = b * cin_pad + ce
+  const long long kdim = (long long)g.nsh * g.cin_pad;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)g.cout_pad * g.cin_pad) return;
-  const int ce = (int)(idx % g.cin_pad);
-  const int coe = (int)(idx / g.cin_pad);
+  if (idx >= (long long)g.cout_pad * kdim) return;
+  const int kk = (int)(idx % kdim);
+  const int coe = (int)(idx / kdim);
+  const int ce = kk % g.cin_pad, blk = kk / g.cin_pad;
+  const int bh = blk / g.nb, bw = blk % g.nb;
   const int R = G.R, Pa = G.Pa;
   double We[kMaxR * kMaxR];
   for (int i = 0; i < R * R; ++i) We[i] = 0.0;
@@ -38,16 +43,19 @@ __global__ void __launch_bounds__(128) filter_transform_kernel(const WT* __restr
     int ci = ce, co = coe, ph = 0, pw = 0;
     if (g.mode == 1) { ci = ce / 4; ph = (ce % 4) / 2; pw = ce % 2; }
     if (g.mode == 2) { const int f = coe / g.Cout; co = coe % g.Cout; ph = f / 2; pw = f % 2; }
-    for (int a = 0; a < g.Kp; ++a)
-      for (int b = 0; b < g.Kp; ++b) {
-        const int th = g.taps[ph][a], tw = g.taps[pw][b];
+    for (int a = 0; a < R; ++a)
+      for (int b = 0; b < R; ++b) {
+        const int ka = bh * R + a, kb = bw * R + b;   // phase-filter taps of this block (zero past Kp: P:106)
+        if (ka >= g.Kp || kb >= g.Kp) continue;
+        const int th = g.taps[ph][ka], tw = g.taps[pw][kb];
         if (th < 0 || tw < 0) continue;
         const long long off = (g.mode == 2) ? (((long long)ci * g.Cout + co) * K + th) * K + tw
                                             : (((long long)co * g.Cin + ci) * K + th) * K + tw;
         We[a * R + b] = ld_w(w, off);
       }
   }
-  const long long plane = (long long)Pa * Pa * g.cout_pad * g.cin_pad;
+  const long long rowlen = (long long)g.cout_pad * kdim;       // elements per point
+  const long long plane = (long long)Pa * Pa * rowlen;
   double t1[kMaxR];
   for (int p1 = 0; p1 < Pa; ++p1) {
     for (int b = 0; b < R; ++b) {
@@ -58,7 +66,7 @@ __global__ void __launch_bounds__(128) filter_transform_kernel(const WT* __restr
     for (int p2 = 0; p2 < Pa; ++p2) {
       double u = 0.0;
       for (int b = 0; b < R; ++b) u += t1[b] * G.g[p2 * R + b];
-      const long long o = ((long long)(p1 * Pa + p2) * g.cout_pad + coe) * g.cin_pad + ce;
+      const long long o = (long long)(p1 * Pa + p2) * rowlen + (long long)coe * kdim + kk;
       if (BF) {
         __nv_bfloat16* U = reinterpret_cast<__nv_bfloat16*>(Uout);
         const __nv_bfloat16 hi = __double2bfloat16(u);
@@ -74,11 +82,12 @@ __global__ void __launch_bounds__(128) filter_transform_kernel(const WT* __restr
 
 nw_status_t launch_filter_transform(const nw_plan_st* p, const Geometry& g, const void* w, void* U, cudaStream_t s) {
   GhatParam G{};
-  G.Pa = p->ax.Pa;
-  G.R = p->ax.R;
+  const NestedAxis ax = path_axis(p, g.path);
+  G.Pa = ax.Pa;
+  G.R = g.R;
   for (int q = 0; q < G.Pa; ++q)
-    for (int k = 0; k < G.R; ++k) G.g[q * G.R + k] = rdouble(g_hat(p->ax, q, k));
-  const long long n = (long long)g.cout_pad * g.cin_pad;
+    for (int k = 0; k < G.R; ++k) G.g[q * G.R + k] = (g.path == kPathDirect) ? 1.0 : rdouble(g_hat(ax, q, k));
+  const long long n = (long long)g.cout_pad * g.nsh * g.cin_pad;
   const int blocks = (int)((n + 127) / 128);
   const bool bf = p->math != NW_MATH_FP32_SIMT;
   LaunchScope scope_("filter_transform", s);

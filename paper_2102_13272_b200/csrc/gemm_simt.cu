@@ -7,20 +7,31 @@ namespace nw {
 // G3s: FP32 SIMT contraction, batched over transform points
 // M[xi][co][t] = sum_k V[xi][t][k] * U[xi][co][k]
 // ---------------------------------------------------------------------------
+struct Shifts {
+  int nsh, cin_pad;
+  int off[kMaxShift];
+};
+
+// K = nsh * cin_pad: k-range of shift s reads A rows t + off[s] (OLA / direct
+// comparison paths); rows past the point's T_pad read as zero.
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict__ V, const float* __restrict__ U,
-                                                        float* __restrict__ M, long long T_pad, int K, int Nn) {
+                                                        float* __restrict__ M, long long T_pad, int K, int Nn,
+                                                        const __grid_constant__ Shifts sh) {
   __shared__ float As[16][64 + 4];
   __shared__ float Bs[16][64 + 4];
   const int xi = blockIdx.z;
   const long long t0 = (long long)blockIdx.x * 64;
   const int n0 = blockIdx.y * 64;
   const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
-  const float* Vb = V + ((long long)xi * T_pad + t0) * K;
+  const float* Vb = V + (long long)xi * T_pad * sh.cin_pad;
   const float* Ub = U + ((long long)xi * Nn + n0) * K;
   float acc[4][4] = {};
   const int lr = tid / 4, lk = (tid % 4) * 4;
   for (int k0 = 0; k0 < K; k0 += 16) {
-    const float4 a = *reinterpret_cast<const float4*>(Vb + (long long)lr * K + k0 + lk);
+    const int s = k0 / sh.cin_pad, kc = k0 - s * sh.cin_pad;
+    const long long row = t0 + lr + sh.off[s];
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row < T_pad) a = *reinterpret_cast<const float4*>(Vb + row * sh.cin_pad + kc + lk);
     float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
     if (n0 + lr < Nn) bb = *reinterpret_cast<const float4*>(Ub + (long long)lr * K + k0 + lk);
     As[lk + 0][lr] = a.x; As[lk + 1][lr] = a.y; As[lk + 2][lr] = a.z; As[lk + 3][lr] = a.w;
@@ -56,7 +67,12 @@ nw_status_t launch_gemm_simt(const nw_plan_st* p, const Geometry& g, const float
   (void)p;
   dim3 grid((unsigned)(g.T_pad / 64), (unsigned)((g.cout_pad + 63) / 64), (unsigned)g.P);
   LaunchScope scope_("contraction_fp32_simt", s);
-  gemm_simt_kernel<<<grid, 256, 0, s>>>(V, U, M, g.T_pad, g.cin_pad, g.cout_pad);
+  Shifts sh{};
+  if (g.nsh < 1 || g.nsh > kMaxShift) return NW_ERR_UNSUPPORTED;
+  sh.nsh = g.nsh;
+  sh.cin_pad = g.cin_pad;
+  for (int b = 0; b < g.nsh; ++b) sh.off[b] = (b / g.nb) * g.tiles_w + (b % g.nb);
+  gemm_simt_kernel<<<grid, 256, 0, s>>>(V, U, M, g.T_pad, g.nsh * g.cin_pad, g.cout_pad, sh);
   return check_launch();
 }
 

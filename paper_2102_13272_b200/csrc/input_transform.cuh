@@ -211,7 +211,7 @@ static nw_status_t input_pick(const Geometry& g, const void* x, void* V, cudaStr
 // bf16 storage are built for the combos the BASELINE configs use.
 template <int MO, int RO, int MI>
 nw_status_t input_impl(const nw_plan_st* p, const Geometry& g, const void* x, void* V, cudaStream_t s) {
-  constexpr bool kFull = (MO == 3 && RO == 3 && MI == 3);
+  constexpr bool kFull = (MO == 3 && RO == 3 && MI == 3) || (MO == 1 && RO == 1 && MI == 3);  // nested / OLA
   constexpr bool kBf16In = kFull || (MO == 2 && RO == 3 && MI == 2);
   const bool bf = p->math != NW_MATH_FP32_SIMT;
   const bool xb = p->dtype == NW_DTYPE_BF16;

@@ -33,7 +33,16 @@ struct Geometry {
   long long T, T_pad;       // slices, padded to the GEMM M tile
   int cin_e, cout_e, cin_pad, cout_pad;
   int P, Pa;
+  // path (nested / OLA comparison / direct comparison) and its slice algorithm
+  int path;          // kPathNested, kPathOla, kPathDirect
+  int mo, ro, mi;    // axis kernel F(mo, ro) (x) F(mi, 3): nested = the plan's; OLA = (1, 1, 3); direct: unused
+  int R;             // filter taps per block and axis (3 r_o nested, 3 OLA, 1 direct)
+  int nb;            // filter blocks per axis: 1 nested, ceil(Kp/3) OLA (Eq. 2.3), Kp direct (Eq. 2.1 taps)
+  int nsh;           // nb^2: contraction K = nsh * cin_pad, A rows shifted per block
 };
+
+constexpr int kPathNested = 0, kPathOla = 1, kPathDirect = 2;
+constexpr int kMaxShift = 81;
 
 }  // namespace nw
 
@@ -54,14 +63,19 @@ namespace nw {
 extern std::atomic<unsigned long long> g_launches;
 
 nw_status_t finalize(nw_plan_st *p);
-Geometry make_geometry(const nw_plan_st *p, int N, int H, int W);
+Geometry make_geometry(const nw_plan_st *p, int N, int H, int W, int path = kPathNested);
 size_t v_bytes(const nw_plan_st *p, const Geometry &g);
 size_t m_bytes(const nw_plan_st *p, const Geometry &g);
+size_t u_bytes(const Geometry &g);  // P * cout_pad * nsh * cin_pad * 4
 size_t filter_bytes(const nw_plan_st *p);
+NestedAxis path_axis(const nw_plan_st *p, int path);
 
 // launchers (nested_kernels.cu)
 nw_status_t launch_filter_transform(const nw_plan_st *p, const Geometry &g, const void *w, void *U,
                                     cudaStream_t s);
+// direct comparison path (comparison.cu): NCHW x -> shifted-pixel-grid V; M -> y
+nw_status_t launch_pack_input(const nw_plan_st *p, const Geometry &g, const void *x, void *V, cudaStream_t s);
+nw_status_t launch_unpack_output(const nw_plan_st *p, const Geometry &g, const float *M, void *y, cudaStream_t s);
 nw_status_t launch_input_transform(const nw_plan_st *p, const Geometry &g, const void *x, void *V,
                                    cudaStream_t s);
 nw_status_t launch_output_transform(const nw_plan_st *p, const Geometry &g, const float *M, void *y,

@@ -89,15 +89,34 @@ nw_status_t finalize(nw_plan_st *p) {
   return NW_OK;
 }
 
-Geometry make_geometry(const nw_plan_st *p, int N, int H, int W) {
+NestedAxis path_axis(const nw_plan_st *p, int path) {
+  if (path == kPathNested) return p->ax;
+  if (path == kPathOla) return make_axis(1, 1, kRi);  // single-level F(3,3) = F(1,1) (x) F(3,3)
+  NestedAxis A{};                                      // direct: no transform, one point, pixel tiles
+  A.m_o = A.r_o = A.m_i = 1;
+  A.l_o = A.l_i = A.Pa = A.L = A.Ma = A.R = 1;
+  A.adv = 1;
+  A.nph = 1;
+  return A;
+}
+
+// Slice geometry of one path.  Nested: slices of adv x adv outputs.
+// OLA (Eq. 2.3): 3x3-output F(3,3) tiles; the nb x nb filter blocks read the
+// tile grid shifted by (bh, bw), so the grid is extended by nb - 1 tiles per
+// axis and block b's operand is V row t + bh * tiles_w + bw.  Direct (Eq. 2.1):
+// one "tile" per pixel of the (phase) input grid extended by Kp - 1; tap
+// (a, b) reads pixel row t + a * tiles_w + b.
+Geometry make_geometry(const nw_plan_st *p, int N, int H, int W, int path) {
   Geometry g{};
   int off[2];
   phase_split(p, &g.mode, &g.n_sp, &g.Kp, off, g.taps);
   g.SR = (g.mode == 1) ? 2 : 1;
   for (int a = 0; a < 2; ++a) g.off[a] = (g.mode == 2) ? -off[a] : off[a];
-  g.adv = p->ax.adv;
-  g.nph = p->ax.nph;
-  for (int i = 0; i < 3; ++i) g.shift[i] = p->ax.shift[i];
+  const NestedAxis ax = path_axis(p, path);
+  g.path = path;
+  g.adv = ax.adv;
+  g.nph = ax.nph;
+  for (int i = 0; i < 3; ++i) g.shift[i] = ax.shift[i];
   g.N = N; g.Cin = p->Cin; g.Cout = p->Cout; g.H = H; g.W = W;
   if (g.mode == 2) {
     g.Ho = (H - 1) * 2 - 2 * p->pad + p->K + p->output_padding;
@@ -112,11 +131,27 @@ Geometry make_geometry(const nw_plan_st *p, int N, int H, int W) {
   }
   g.tiles_h = (g.Hq + g.adv - 1) / g.adv;
   g.tiles_w = (g.Wq + g.adv - 1) / g.adv;
+  if (path == kPathNested) {
+    g.mo = p->m_o; g.ro = p->r_o; g.mi = p->m_i;
+    g.R = kRi * p->r_o;
+    g.nb = 1;
+  } else if (path == kPathOla) {
+    g.mo = 1; g.ro = 1; g.mi = kRi;
+    g.R = kRi;
+    g.nb = (g.Kp + kRi - 1) / kRi;
+  } else {
+    g.mo = g.ro = g.mi = 1;
+    g.R = 1;
+    g.nb = g.Kp;
+  }
+  g.tiles_h += g.nb - 1;
+  g.tiles_w += g.nb - 1;
+  g.nsh = g.nb * g.nb;
   g.T = (long long)N * g.tiles_h * g.tiles_w * g.nph * g.nph;
   g.T_pad = round_up(g.T, 128);
   g.cin_e = p->cin_e; g.cout_e = p->cout_e;
   g.cin_pad = p->cin_pad; g.cout_pad = p->cout_pad;
-  g.Pa = p->ax.Pa;
+  g.Pa = ax.Pa;
   g.P = g.Pa * g.Pa;
   return g;
 }
@@ -129,6 +164,9 @@ size_t v_bytes(const nw_plan_st *p, const Geometry &g) {
 size_t m_bytes(const nw_plan_st *p, const Geometry &g) {
   (void)p;
   return (size_t)round_up((long long)g.P * g.T_pad * g.cout_pad * 4, 256);
+}
+size_t u_bytes(const Geometry &g) {
+  return (size_t)round_up((long long)g.P * g.cout_pad * g.nsh * g.cin_pad * 4, 256);
 }
 size_t filter_bytes(const nw_plan_st *p) {
   const long long P = (long long)p->ax.Pa * p->ax.Pa;

@@ -90,6 +90,11 @@ struct Params {
   long long a_lo_row; // row offset of the lo plane in the V tensor map (= P * T_pad)
   long long b_lo_row; // row offset of the lo plane in the U tensor map (= P * N)
   float* M;
+  // shifted operands (OLA / direct comparison paths): k-block kb belongs to
+  // shift s = kb / kbc and channel block kc = kb % kbc; its A rows are read at
+  // t + shoff[s] and its B columns at s * cin_pad + kc * 64.  Nested: nsh = 1.
+  int nsh, kbc, cin_pad;
+  int shoff[kMaxShift];
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -153,17 +158,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t bfull = smem_u32(&B_full[sb]);
           mbar_expect_tx(bfull, b_stage);
           const uint32_t bdst = base + b_off + sb * b_stage;
-          tma_load_2d(bdst, &mapU, bfull, kb * kBK, xi * p.N);
-          if (p.lo) tma_load_2d(bdst + b_plane, &mapU, bfull, kb * kBK, (int)(p.b_lo_row + (long long)xi * p.N));
+          const int sh = kb / p.kbc, kc = kb - sh * p.kbc;
+          const int bcol = sh * p.cin_pad + kc * kBK, acol = kc * kBK, aoff = p.shoff[sh];
+          tma_load_2d(bdst, &mapU, bfull, bcol, xi * p.N);
+          if (p.lo) tma_load_2d(bdst + b_plane, &mapU, bfull, bcol, (int)(p.b_lo_row + (long long)xi * p.N));
           if (++sb == p.nB) { sb = 0; pb ^= 1; }
           for (int g = 0; g < g_eff; ++g) {
             mbar_wait(smem_u32(&A_empty[sa]), pa ^ 1);
             const uint32_t afull = smem_u32(&A_full[sa]);
             mbar_expect_tx(afull, a_stage);
             const uint32_t adst = base + a_off + sa * a_stage;
-            const long long row = (long long)xi * p.T_pad + (long long)(mb0 + g) * kBM;
-            tma_load_2d(adst, &mapV, afull, kb * kBK, (int)row);
-            if (p.lo) tma_load_2d(adst + a_plane, &mapV, afull, kb * kBK, (int)(p.a_lo_row + row));
+            const long long row = (long long)xi * p.T_pad + (long long)(mb0 + g) * kBM + aoff;
+            tma_load_2d(adst, &mapV, afull, acol, (int)row);
+            if (p.lo) tma_load_2d(adst + a_plane, &mapV, afull, acol, (int)(p.a_lo_row + row));
             if (++sa == p.nA) { sa = 0; pa ^= 1; }
           }
         }
@@ -271,7 +278,12 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   if (prm.G > 4) prm.G = 4;
   if (prm.G < 1) prm.G = 1;
   prm.ngrp = (prm.nmb + prm.G - 1) / prm.G;
-  prm.KB = (g.cin_pad + tc::kBK - 1) / tc::kBK;
+  if (g.nsh < 1 || g.nsh > kMaxShift) return NW_ERR_UNSUPPORTED;
+  prm.nsh = g.nsh;
+  prm.kbc = (g.cin_pad + tc::kBK - 1) / tc::kBK;
+  prm.cin_pad = g.cin_pad;
+  prm.KB = prm.nsh * prm.kbc;
+  for (int b = 0; b < g.nsh; ++b) prm.shoff[b] = (b / g.nb) * g.tiles_w + (b % g.nb);  // Eq. 2.3 block shift
   prm.lo = (p->math == NW_MATH_BF16X3) ? 1 : 0;
   prm.T_pad = g.T_pad;
   prm.a_lo_row = (long long)g.P * g.T_pad;
@@ -296,7 +308,7 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   if (rowsV >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
   alignas(64) CUtensorMap mapV, mapU;
   if (!make_map(&mapV, V, rowsV, g.cin_pad, tc::kBM)) return NW_ERR_CUDA;
-  if (!make_map(&mapU, U, rowsU, g.cin_pad, prm.N)) return NW_ERR_CUDA;
+  if (!make_map(&mapU, U, rowsU, (long long)g.nsh * g.cin_pad, prm.N)) return NW_ERR_CUDA;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(tc::contraction_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=

@@ -91,3 +91,26 @@ def test_output_sizes():
     assert _lib.Plan(7, 2, 3, 3, 3, 64, pad=3).output_size(224, 224) == (112, 112)
     assert _lib.Plan(9, 2, 3, 3, 64, 64, pad=4).output_size(112, 112) == (56, 56)
     assert _lib.Plan(9, 1, 3, 3, 256, 256, pad=4).output_size(64, 64) == (64, 64)
+
+
+def _r256(b):
+    return (b + 255) // 256 * 256
+
+
+@pytest.mark.parametrize("K,pad", [(5, 2), (7, 3), (9, 4)])
+def test_comparison_workspace_geometry(K, pad):
+    # OLA (Eq. 2.3): ceil(K/3)^2 blocks of F(3,3) over a 3x3-output tile grid extended by nb-1;
+    # direct (Eq. 2.1): K^2 taps over the pixel grid extended by K-1.  Sizes = U + V + M, 4 B/elt.
+    N, C, H = 2, 64, 40
+    plan = _lib.Plan(K, 1, 3, 3, C, C, pad=pad)
+    nb = -(-K // 3)
+    tiles = -(-H // 3) + nb - 1
+    T = N * tiles * tiles
+    Tp = -(-T // 128) * 128
+    ola = _r256(25 * C * nb * nb * C * 4) + 2 * _r256(25 * Tp * C * 4)
+    assert plan.workspace_size(N, H, H, "ola") == ola
+    px = H + K - 1
+    T = N * px * px
+    Tp = -(-T // 128) * 128
+    direct = _r256(C * K * K * C * 4) + 2 * _r256(Tp * C * 4)
+    assert plan.workspace_size(N, H, H, "direct") == direct
