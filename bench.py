@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--workload", default="c2", choices=list(WORKLOADS))
     ap.add_argument("--math", default="bf16x3", choices=["bf16x3", "fp32", "bf16"])
     ap.add_argument("--path", default="nested", choices=["nested", "ola", "direct"])
+    ap.add_argument("--m-outer", type=int, default=None,
+                    help="outer kernel F(m,3) of the nested plan (default: the config's, 3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-compare", action="store_true", help="skip the OLA / direct comparison lines")
@@ -160,7 +162,7 @@ def kernel_work(layer, info, math):
     }
 
 
-def roofline(prof, works, math, peaks, steps):
+def roofline(prof, works, math, peaks, steps, layers):
     """Pick the kernel with the largest total time; achieved = algorithmic work / mean launch time."""
     if not prof:
         return None
@@ -178,10 +180,15 @@ def roofline(prof, works, math, peaks, steps):
         tpeak = None
     t_bytes = bytes_per_launch / (hbm * 1e9)
     t_flops = flops_per_launch / (tpeak * 1e12) if tpeak else 0.0
+    # ncu dram read+write bytes per launch of this kernel, averaged over the workload's
+    # layers (profiles/traffic.json, written by tools/ncu_summary.py); null if any is missing
     trafile = os.path.join(ROOT, "profiles", "traffic.json")
     traffic = None
     if os.path.exists(trafile):
-        traffic = json.load(open(trafile)).get(f"{kind}:{math}")
+        tab = json.load(open(trafile))
+        vals = [tab.get(f"{kind}:{math}:{l.name}:m{l.m_o}") for l in layers]
+        if vals and all(v is not None for v in vals):
+            traffic = int(sum(vals) / len(vals))
     if t_flops > t_bytes:
         bound = "tensor" if kind == "contraction_tc" else "alu"
         achieved = flops_per_launch / avg_s / 1e12
@@ -241,6 +248,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     layers_all = [synth.CONFIGS[n] for n in WORKLOADS[args.workload]]
+    if args.m_outer:
+        layers_all = [l.with_(m_o=args.m_outer) if l.m_i == 3 else l for l in layers_all]
 
     if args.impl == "reference":
         return reference_arm(args, layers_all, world, rank)
@@ -250,6 +259,7 @@ def main():
 
     import paper_2102_13272_b200 as nw
     from paper_2102_13272_b200 import _lib
+    from paper_2102_13272_b200 import dist as nwd
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -274,8 +284,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         filt_ms += e0.elapsed_time(e1)
-        if world > 1:
-            dist.broadcast(conv.U, src=0)
+        nwd.broadcast_filter(conv.U, src=0)   # the one collective: U from rank 0 (NCCL / NVLink)
         x = t["x"].to(dev)
         y = torch.empty(conv.out_shape(x.shape), dtype=x.dtype, device=dev)
         conv.workspace(*x.shape[:1], *x.shape[2:], path=args.path)
@@ -310,11 +319,7 @@ def main():
     if world > 1:
         dist.barrier()
     launches = nw.launch_count() - launches0
-    ms = start.elapsed_time(end)
-    if world > 1:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = nwd.max_over_ranks(start.elapsed_time(end), dev)
     ms_step = ms / args.steps
     flops_rank = sum(l.direct_flops() for l in layers_all)
     value = flops_rank * world / (ms_step / 1e3) / 1e12
@@ -385,17 +390,13 @@ def main():
             e2e_step()
         s1.record(stream)
         torch.cuda.synchronize()
-        ems = s0.elapsed_time(s1) / ek
-        if world > 1:
-            tt = torch.tensor([ems], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
+        ems = nwd.max_over_ranks(s0.elapsed_time(s1) / ek, dev)
         e2e = {"value": round(flops_rank * world / (ems / 1e3) / 1e12, 3), "unit": "TFLOP/s",
                "ms_per_step": round(ems, 3),
                "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in xs)),
                "d2h_bytes_per_step": int(sum(y.numel() * y.element_size() for y in ys))}
 
-    roof = roofline(prof, works, args.math, peaks, args.steps)
+    roof = roofline(prof, works, args.math, peaks, args.steps, layers_all)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -412,6 +413,7 @@ def main():
             "dtype": {"bf16x3": "bf16x3", "fp32": "f32", "bf16": "bf16"}[args.math],
             "data": "synthetic (seeded; BASELINE distributions, DESIGN.md input recipe)",
             "config": {"workload": WORKLOAD_DESC[args.workload], "layers": [l.name for l in layers_all],
+                       "nesting": [f"F({l.m_o},3)(x)F({l.m_i},3)" for l in layers_all],
                        "path": args.path, "math": args.math, "images_per_rank": layers_all[0].N,
                        "l2": "no flush: x (>=134 MB) and V/M (>1 GB per layer) exceed the 126 MB L2",
                        "step": "input transform + contraction + output transform per layer (nw_conv_forward)"},

@@ -1,6 +1,9 @@
 // api.cu -- device-side half of the C ABI: argument checks, workspace carving
 // and the launch sequence of each path.  Every path is our own kernels; there
 // is no CPU or library fallback (a missing kernel returns NW_ERR_UNSUPPORTED).
+#include <cstdlib>
+#include <vector>
+
 #include "nw_internal.h"
 
 using namespace nw;
@@ -20,42 +23,163 @@ nw_status_t nw_transform_filter(nw_plan_t p, const void *w, void *U, nw_stream_t
   return launch_filter_transform(p, g, w, U, reinterpret_cast<cudaStream_t>(stream));
 }
 
+}  // extern "C"
+
+namespace nw {
+
+static int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
+// Chunk pipeline of the forward pass: the batch is cut into k chunks; chunk c's
+// input transform, contraction and output transform run on three streams, so
+// the CUDA-core transforms of one chunk overlap the HBM-bound tensor-core
+// contraction of the next.  V / M are double buffered.
+int forward_chunks(const nw_plan_st *p, int N, int H, int W) {
+  int k = p->pipe_chunks >= 0 ? p->pipe_chunks : env_int("NW_PIPE_CHUNKS", 1);
+  if (k > N) k = N;
+  if (k < 1) k = 1;
+  Geometry g = make_geometry(p, 1, H, W);
+  const size_t es = (p->dtype == NW_DTYPE_BF16) ? 2 : 4;
+  // chunk pointers must stay 16-byte aligned
+  if (((size_t)p->Cin * H * W * es) % 16 || ((size_t)p->Cout * g.Ho * g.Wo * es) % 16) k = 1;
+  return k;
+}
+
+size_t forward_ws_bytes(const nw_plan_st *p, int N, int H, int W) {
+  const int k = forward_chunks(p, N, H, W);
+  const int nc = (N + k - 1) / k;
+  Geometry g = make_geometry(p, nc, H, W);
+  return (size_t)(k > 1 ? 2 : 1) * (v_bytes(p, g) + m_bytes(p, g));
+}
+
+static nw_status_t forward_one(const nw_plan_st *p, const Geometry &g, const void *x, const void *U, void *y, void *V,
+                               float *M, cudaStream_t si, cudaStream_t sg, cudaStream_t so, cudaEvent_t e_in,
+                               cudaEvent_t e_gemm) {
+  nw_status_t st;
+  if ((st = launch_input_transform(p, g, x, V, si)) != NW_OK) return st;
+  if (si != sg) {
+    if (cudaEventRecord(e_in, si) != cudaSuccess || cudaStreamWaitEvent(sg, e_in, 0) != cudaSuccess) return NW_ERR_CUDA;
+  }
+  if (p->math == NW_MATH_FP32_SIMT)
+    st = launch_gemm_simt(p, g, static_cast<const float *>(V), static_cast<const float *>(U), M, sg);
+  else
+    st = launch_gemm_tc(p, g, V, U, M, sg);
+  if (st != NW_OK) return st;
+  if (sg != so) {
+    if (cudaEventRecord(e_gemm, sg) != cudaSuccess || cudaStreamWaitEvent(so, e_gemm, 0) != cudaSuccess)
+      return NW_ERR_CUDA;
+  }
+  return launch_output_transform(p, g, M, y, so);
+}
+
+}  // namespace nw
+
+extern "C" {
+
 nw_status_t nw_conv_forward(nw_plan_t p, const void *x, const void *U, void *y, int N, int H, int W, void *ws,
                             size_t ws_bytes, nw_stream_t stream) {
   if (!p || !x || !U || !y || N < 1 || H < 1 || W < 1) return NW_ERR_INVALID;
   nw_status_t st = finalize(p);
   if (st != NW_OK) return st;
   if (!aligned16(x) || !aligned16(U) || !aligned16(y) || !aligned16(ws)) return NW_ERR_INVALID;
-  Geometry g = make_geometry(p, N, H, W);
-  if (g.Ho < 1 || g.Wo < 1) return NW_ERR_INVALID;
-  const size_t vb = v_bytes(p, g), mb = m_bytes(p, g);
-  if (!ws || ws_bytes < vb + mb) return NW_ERR_WORKSPACE;
+  Geometry gfull = make_geometry(p, N, H, W);
+  if (gfull.Ho < 1 || gfull.Wo < 1) return NW_ERR_INVALID;
+  if (!ws || ws_bytes < forward_ws_bytes(p, N, H, W)) return NW_ERR_WORKSPACE;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int k = forward_chunks(p, N, H, W);
   char *base = static_cast<char *>(ws);
-  void *V = base;
-  float *M = reinterpret_cast<float *>(base + vb);
-  if ((st = launch_input_transform(p, g, x, V, s)) != NW_OK) return st;
-  if (p->math == NW_MATH_FP32_SIMT)
-    st = launch_gemm_simt(p, g, static_cast<const float *>(V), static_cast<const float *>(U), M, s);
-  else
-    st = launch_gemm_tc(p, g, V, U, M, s);
+  if (k == 1) {
+    const size_t vb = v_bytes(p, gfull);
+    return forward_one(p, gfull, x, U, y, base, reinterpret_cast<float *>(base + vb), s, s, s, nullptr, nullptr);
+  }
+  const int nc = (N + k - 1) / k;
+  const int nchunks = (N + nc - 1) / nc;
+  Geometry gc = make_geometry(p, nc, H, W);
+  gc.gemm_ctas = env_int("NW_GEMM_CTAS", 0);
+  const size_t vb = v_bytes(p, gc), mb = m_bytes(p, gc);
+  const size_t es = (p->dtype == NW_DTYPE_BF16) ? 2 : 4;
+  const size_t ximg = (size_t)p->Cin * H * W * es, yimg = (size_t)p->Cout * gfull.Ho * gfull.Wo * es;
+  {
+    std::lock_guard<std::mutex> lk(p->io_mu);
+    for (auto &ps : p->s_pipe)
+      if (!ps && cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking) != cudaSuccess) return NW_ERR_CUDA;
+  }
+  cudaStream_t si = p->s_pipe[0], sg = p->s_pipe[1], so = p->s_pipe[2];
+  // events: start, then per chunk in / gemm / out
+  std::vector<cudaEvent_t> ev(1 + 3 * (size_t)nchunks, nullptr);
+  for (auto &e : ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return NW_ERR_CUDA;
+  auto E_in = [&](int c) { return ev[1 + 3 * c]; };
+  auto E_gemm = [&](int c) { return ev[2 + 3 * c]; };
+  auto E_out = [&](int c) { return ev[3 + 3 * c]; };
+  bool ok = cudaEventRecord(ev[0], s) == cudaSuccess;
+  for (cudaStream_t t : {si, sg, so}) ok = ok && cudaStreamWaitEvent(t, ev[0], 0) == cudaSuccess;
+  for (int c = 0; ok && st == NW_OK && c < nchunks; ++c) {
+    const int n0 = c * nc, nk = (N - n0) < nc ? (N - n0) : nc, b = c & 1;
+    Geometry g = (nk == nc) ? gc : make_geometry(p, nk, H, W);
+    g.gemm_ctas = gc.gemm_ctas;
+    char *V = base + (size_t)b * (vb + mb);
+    float *M = reinterpret_cast<float *>(V + vb);
+    if (c >= 2) {  // buffer b: V read by contraction c-2, M read by output transform c-2
+      ok = ok && cudaStreamWaitEvent(si, E_gemm(c - 2), 0) == cudaSuccess;
+      ok = ok && cudaStreamWaitEvent(sg, E_out(c - 2), 0) == cudaSuccess;
+    }
+    if (!ok) break;
+    st = forward_one(p, g, static_cast<const char *>(x) + (size_t)n0 * ximg, U,
+                     static_cast<char *>(y) + (size_t)n0 * yimg, V, M, si, sg, so, E_in(c), E_gemm(c));
+    ok = ok && cudaEventRecord(E_out(c), so) == cudaSuccess;
+  }
+  if (ok && st == NW_OK) ok = cudaStreamWaitEvent(s, E_out(nchunks - 1), 0) == cudaSuccess;
+  for (auto &e : ev) cudaEventDestroy(e);
   if (st != NW_OK) return st;
-  return launch_output_transform(p, g, M, y, s);
+  return ok ? NW_OK : NW_ERR_CUDA;
 }
 
 }  // extern "C"
 
 extern "C" {
 
+// Host-buffer forward, pipelined: the batch is cut into chunks of nc images;
+// chunk k's x is copied host -> device on a copy stream while chunk k-1 runs
+// the nested forward on `stream` and chunk k-2's y is copied device -> host on
+// a second copy stream (PCIe is full duplex).  x and y chunks are double
+// buffered in the workspace; events order reuse.  The call stays asynchronous:
+// `stream` waits for the last device -> host copy before anything enqueued
+// after this call.
+static int host_chunk(int N) {
+  int nc = (N + 7) / 8;         // <= 8 chunks
+  if (nc < 2) nc = N < 2 ? N : 2;
+  return nc;
+}
+
+static void host_layout(const nw_plan_st *p, int N, int H, int W, size_t *fw, size_t *xb, size_t *yb, int *nc) {
+  *nc = host_chunk(N);
+  Geometry g = make_geometry(p, *nc, H, W);
+  const size_t es = (p->dtype == NW_DTYPE_BF16) ? 2 : 4;
+  *fw = forward_ws_bytes(p, *nc, H, W);
+  *xb = (size_t)round_up((long long)*nc * p->Cin * H * W * es, 256);
+  *yb = (size_t)round_up((long long)*nc * p->Cout * g.Ho * g.Wo * es, 256);
+}
+
+nw_plan_st::~nw_plan_st() {
+  if (s_h2d) cudaStreamDestroy(s_h2d);
+  if (s_d2h) cudaStreamDestroy(s_d2h);
+  for (auto &ps : s_pipe)
+    if (ps) cudaStreamDestroy(ps);
+}
+
 nw_status_t nw_workspace_size_host(nw_plan_t p, int N, int H, int W, size_t *bytes) {
-  size_t b = 0;
-  nw_status_t st = nw_workspace_size(p, N, H, W, &b);
+  if (!p || !bytes || N < 1 || H < 1 || W < 1) return NW_ERR_INVALID;
+  nw_status_t st = finalize(p);
   if (st != NW_OK) return st;
   Geometry g = make_geometry(p, N, H, W);
-  const size_t es = (p->dtype == NW_DTYPE_BF16) ? 2 : 4;
-  const size_t xb = (size_t)round_up((long long)N * p->Cin * H * W * es, 256);
-  const size_t yb = (size_t)round_up((long long)N * p->Cout * g.Ho * g.Wo * es, 256);
-  *bytes = b + xb + yb;
+  if (g.Ho < 1 || g.Wo < 1) return NW_ERR_INVALID;
+  size_t fw, xb, yb;
+  int nc;
+  host_layout(p, N, H, W, &fw, &xb, &yb, &nc);
+  *bytes = fw + 2 * xb + 2 * yb;
   return NW_OK;
 }
 
@@ -66,20 +190,51 @@ nw_status_t nw_conv_forward_host(nw_plan_t p, const void *x_host, const void *U,
   nw_status_t st = nw_workspace_size_host(p, N, H, W, &need);
   if (st != NW_OK) return st;
   if (!ws || ws_bytes < need) return NW_ERR_WORKSPACE;
+  size_t fw, xb, yb;
+  int nc;
+  host_layout(p, N, H, W, &fw, &xb, &yb, &nc);
   Geometry g = make_geometry(p, N, H, W);
   const size_t es = (p->dtype == NW_DTYPE_BF16) ? 2 : 4;
-  const size_t xbytes = (size_t)N * p->Cin * H * W * es;
-  const size_t ybytes = (size_t)N * p->Cout * g.Ho * g.Wo * es;
-  const size_t fw = v_bytes(p, g) + m_bytes(p, g);
+  const size_t ximg = (size_t)p->Cin * H * W * es, yimg = (size_t)p->Cout * g.Ho * g.Wo * es;
   char *base = static_cast<char *>(ws);
-  char *xd = base + fw;
-  char *yd = xd + (size_t)round_up((long long)xbytes, 256);
+  char *xd[2] = {base + fw, base + fw + xb};
+  char *yd[2] = {base + fw + 2 * xb, base + fw + 2 * xb + yb};
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (cudaMemcpyAsync(xd, x_host, xbytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return NW_ERR_CUDA;
-  st = nw_conv_forward(p, xd, U, yd, N, H, W, ws, fw, stream);
+  {
+    std::lock_guard<std::mutex> lk(p->io_mu);
+    if (!p->s_h2d && cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking) != cudaSuccess) return NW_ERR_CUDA;
+    if (!p->s_d2h && cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking) != cudaSuccess) return NW_ERR_CUDA;
+  }
+  const int nchunks = (N + nc - 1) / nc;
+  // events: [0] start, per chunk: in (x landed), comp (forward done), out (y copied)
+  std::vector<cudaEvent_t> ev(1 + 3 * (size_t)nchunks, nullptr);
+  for (auto &e : ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return NW_ERR_CUDA;
+  auto E_in = [&](int k) { return ev[1 + 3 * k]; };
+  auto E_comp = [&](int k) { return ev[2 + 3 * k]; };
+  auto E_out = [&](int k) { return ev[3 + 3 * k]; };
+  bool ok = cudaEventRecord(ev[0], s) == cudaSuccess && cudaStreamWaitEvent(p->s_h2d, ev[0], 0) == cudaSuccess &&
+            cudaStreamWaitEvent(p->s_d2h, ev[0], 0) == cudaSuccess;
+  for (int k = 0; ok && k < nchunks; ++k) {
+    const int n0 = k * nc, nk = (N - n0) < nc ? (N - n0) : nc, b = k & 1;
+    if (k >= 2) ok = ok && cudaStreamWaitEvent(p->s_h2d, E_comp(k - 2), 0) == cudaSuccess;  // x buffer free
+    ok = ok && cudaMemcpyAsync(xd[b], static_cast<const char *>(x_host) + (size_t)n0 * ximg, (size_t)nk * ximg,
+                               cudaMemcpyHostToDevice, p->s_h2d) == cudaSuccess;
+    ok = ok && cudaEventRecord(E_in(k), p->s_h2d) == cudaSuccess;
+    ok = ok && cudaStreamWaitEvent(s, E_in(k), 0) == cudaSuccess;
+    if (k >= 2) ok = ok && cudaStreamWaitEvent(s, E_out(k - 2), 0) == cudaSuccess;  // y buffer free
+    if (!ok) break;
+    st = nw_conv_forward(p, xd[b], U, yd[b], nk, H, W, ws, fw, stream);
+    if (st != NW_OK) break;
+    ok = cudaEventRecord(E_comp(k), s) == cudaSuccess && cudaStreamWaitEvent(p->s_d2h, E_comp(k), 0) == cudaSuccess;
+    ok = ok && cudaMemcpyAsync(static_cast<char *>(y_host) + (size_t)n0 * yimg, yd[b], (size_t)nk * yimg,
+                               cudaMemcpyDeviceToHost, p->s_d2h) == cudaSuccess;
+    ok = ok && cudaEventRecord(E_out(k), p->s_d2h) == cudaSuccess;
+  }
+  if (st == NW_OK && ok) ok = cudaStreamWaitEvent(s, E_out(nchunks - 1), 0) == cudaSuccess;
+  for (auto &e : ev) cudaEventDestroy(e);  // released once their work completes
   if (st != NW_OK) return st;
-  if (cudaMemcpyAsync(y_host, yd, ybytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) return NW_ERR_CUDA;
-  return NW_OK;
+  return ok ? NW_OK : NW_ERR_CUDA;
 }
 
 }  // extern "C"

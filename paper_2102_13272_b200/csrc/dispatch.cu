@@ -17,6 +17,8 @@ nw_status_t output_impl(const nw_plan_st*, const Geometry&, const float*, void*,
     if (mo_ == 3 && ro_ == 2 && mi_ == 3) return FN<3, 2, 3>(__VA_ARGS__); \
     if (mo_ == 2 && ro_ == 3 && mi_ == 3) return FN<2, 3, 3>(__VA_ARGS__); \
     if (mo_ == 1 && ro_ == 1 && mi_ == 3) return FN<1, 1, 3>(__VA_ARGS__); \
+    if (mo_ == 4 && ro_ == 3 && mi_ == 3) return FN<4, 3, 3>(__VA_ARGS__); \
+    if (mo_ == 5 && ro_ == 3 && mi_ == 3) return FN<5, 3, 3>(__VA_ARGS__); \
     return NW_ERR_UNSUPPORTED;                                             \
   } while (0)
 

@@ -18,6 +18,8 @@
 // Channels >= Cin (up to cin_pad) are written as zeros: the contraction runs
 // over cin_pad.
 #pragma once
+#include <cstdlib>
+
 #include "transforms.cuh"
 
 namespace nw {
@@ -25,7 +27,7 @@ namespace nw {
 template <int MO, int RO, int MI, int SR, int CC>
 struct InCfg {
   using X = Ax<MO, RO, MI>;
-  static constexpr int TW = 2;                                  // tiles per block along w
+  static constexpr int TW = (X::L <= 17) ? 2 : 1;               // tiles per block along w
   static constexpr int SPAN = (TW - 1) * X::ADV + X::SHMAX + X::L;  // phase-image columns
   static constexpr int WSC = SR * SPAN;                         // raw window columns
   static constexpr int ROWS = SR * (X::SHMAX + X::L);           // raw window rows
@@ -33,7 +35,8 @@ struct InCfg {
   static constexpr int NPAIR = CC * SR * SR / 2;                // ce pairs per block
   static constexpr int HS = X::NPH * SR * X::PA * CC * CSTR;    // floats
   static constexpr size_t SMEM = (size_t)HS * sizeof(float);
-  static constexpr int THREADS = 256;
+  static constexpr int THREADS = (CC * SR >= 64) ? 512 : (CC * SR >= 32) ? 256 : 128;
+  static constexpr int MINB = 512 / THREADS;                    // resident CTAs per SM (registers <= 128)
 };
 
 // Outer level of the w-pass for both channels of a pair, one inner point p_i
@@ -74,7 +77,8 @@ __device__ __forceinline__ void store_row(const float (*za)[Ax<MO, RO, MI>::LI],
 }
 
 template <int MO, int RO, int MI, int SR, int CC, typename XT, bool BF>
-__global__ void __launch_bounds__(256, 2) input_transform_kernel(const XT* __restrict__ x, void* __restrict__ Vout,
+__global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, RO, MI, SR, CC>::MINB)
+    input_transform_kernel(const XT* __restrict__ x, void* __restrict__ Vout,
                                                                  Geometry g, int cgroups, int wgroups) {
   using X = Ax<MO, RO, MI>;
   using C = InCfg<MO, RO, MI, SR, CC>;
@@ -198,12 +202,20 @@ static nw_status_t input_launch(const Geometry& g, const void* x, void* V, cudaS
   return check_launch();
 }
 
-// Channel-group width: 32 source channels (64-byte V segments per plane) when
-// the layer has them, else 16; stride 2 folds 4 phases per channel, so 8.
 template <int MO, int RO, int MI, int SR, typename XT, bool BF>
 static nw_status_t input_pick(const Geometry& g, const void* x, void* V, cudaStream_t s) {
+  // 16 source channels per 128-thread CTA (4 CTAs / SM), or 32 per 256-thread CTA (2 / SM):
+  // NW_IN_CC=32 selects the wide variant where the layer has the channels
+  static const int cc = [] {
+    const char* v = getenv("NW_IN_CC");
+    return v ? atoi(v) : 32;
+  }();
   if (SR == 2) return input_launch<MO, RO, MI, SR, 8, XT, BF>(g, x, V, s);
-  if (Ax<MO, RO, MI>::NPH == 1 && g.cin_pad >= 32) return input_launch<MO, RO, MI, SR, 32, XT, BF>(g, x, V, s);
+  if (Ax<MO, RO, MI>::NPH == 1) {
+    if (cc >= 64 && g.cin_pad >= 64 && InCfg<MO, RO, MI, SR, 64>::SMEM <= 227 * 1024)
+      return input_launch<MO, RO, MI, SR, 64, XT, BF>(g, x, V, s);
+    if (cc >= 32 && g.cin_pad >= 32) return input_launch<MO, RO, MI, SR, 32, XT, BF>(g, x, V, s);
+  }
   return input_launch<MO, RO, MI, SR, 16, XT, BF>(g, x, V, s);
 }
 
@@ -211,7 +223,8 @@ static nw_status_t input_pick(const Geometry& g, const void* x, void* V, cudaStr
 // bf16 storage are built for the combos the BASELINE configs use.
 template <int MO, int RO, int MI>
 nw_status_t input_impl(const nw_plan_st* p, const Geometry& g, const void* x, void* V, cudaStream_t s) {
-  constexpr bool kFull = (MO == 3 && RO == 3 && MI == 3) || (MO == 1 && RO == 1 && MI == 3);  // nested / OLA
+  // stride 2 and bf16 storage are built for the F(m_o,3) (x) F(3,3) plans and the OLA kernel
+  constexpr bool kFull = (RO == 3 && MI == 3 && MO >= 3) || (MO == 1 && RO == 1 && MI == 3);
   constexpr bool kBf16In = kFull || (MO == 2 && RO == 3 && MI == 2);
   const bool bf = p->math != NW_MATH_FP32_SIMT;
   const bool xb = p->dtype == NW_DTYPE_BF16;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
 #include <cstddef>
 #include <cstdint>
 
@@ -39,6 +40,7 @@ struct Geometry {
   int R;             // filter taps per block and axis (3 r_o nested, 3 OLA, 1 direct)
   int nb;            // filter blocks per axis: 1 nested, ceil(Kp/3) OLA (Eq. 2.3), Kp direct (Eq. 2.1 taps)
   int nsh;           // nb^2: contraction K = nsh * cin_pad, A rows shifted per block
+  int gemm_ctas;     // persistent contraction grid (0: one CTA per SM)
 };
 
 constexpr int kPathNested = 0, kPathOla = 1, kPathDirect = 2;
@@ -56,6 +58,13 @@ struct nw_plan_st {
   // derived at finalize
   int Kp = 0, r_o = 0, cin_e = 0, cout_e = 0, cin_pad = 0, cout_pad = 0;
   nw::NestedAxis ax{};
+  // copy streams of nw_conv_forward_host (created on first use, released by nw_plan_destroy)
+  std::mutex io_mu;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  // streams of the chunk pipeline inside nw_conv_forward (input / contraction / output)
+  cudaStream_t s_pipe[3] = {nullptr, nullptr, nullptr};
+  int pipe_chunks = -1;  // batch chunks of the forward pipeline (-1: NW_PIPE_CHUNKS or the default)
+  ~nw_plan_st();
 };
 
 namespace nw {
@@ -69,6 +78,9 @@ size_t m_bytes(const nw_plan_st *p, const Geometry &g);
 size_t u_bytes(const Geometry &g);  // P * cout_pad * nsh * cin_pad * 4
 size_t filter_bytes(const nw_plan_st *p);
 NestedAxis path_axis(const nw_plan_st *p, int path);
+// forward pipeline: chunks of the batch and the workspace of nw_conv_forward
+int forward_chunks(const nw_plan_st *p, int N, int H, int W);
+size_t forward_ws_bytes(const nw_plan_st *p, int N, int H, int W);
 
 // launchers (nested_kernels.cu)
 nw_status_t launch_filter_transform(const nw_plan_st *p, const Geometry &g, const void *w, void *U,

@@ -26,15 +26,22 @@ namespace nw {
 template <int MO, int RO, int MI>
 struct OutCfg {
   using X = Ax<MO, RO, MI>;
-  static constexpr int CO = 8;   // output channels per unit (consumer warps)
+  // Threads keep (part of) the M_a x M_a output tile in registers.  Up to 9 x 9
+  // one thread owns the tile (SPL = 1); larger outer kernels split the output
+  // columns by outer index t into SPL parts of TH outer outputs each.
+  static constexpr int SPL = (X::MA <= 9) ? 1 : (MO <= 4 ? 2 : 3);
+  static constexpr int TH = (MO + SPL - 1) / SPL;   // outer outputs per part
+  static constexpr int QW = (SPL == 1) ? X::MA : TH * MI;  // output columns per thread
+  static constexpr int CO = (SPL == 1) ? 8 : (SPL == 2 ? 4 : 3);  // output channels per unit
+  static constexpr int WARPS = CO * SPL;          // consumer warps
   static constexpr int TS = 32;  // slices per unit (lanes)
   static constexpr int NST = 4;  // ring depth (point rows)
   static constexpr int STAGE = X::PA * CO * TS;     // floats per ring stage
-  static constexpr int YST = TS * X::MA * X::MA + 1; // floats per warp output stage
-  static constexpr int THREADS = (CO + 1) * 32;
+  static constexpr int YST = TS * X::MA * QW + 1;   // floats per warp output stage
+  static constexpr int THREADS = (WARPS + 1) * 32;
   static constexpr size_t RING_BYTES = (size_t)NST * STAGE * 4;
-  static constexpr size_t YST_BYTES = (size_t)CO * YST * 4;
-  static constexpr size_t INFO_BYTES = (size_t)CO * TS * 16;
+  static constexpr size_t YST_BYTES = ((size_t)WARPS * YST * 4 + 127) / 128 * 128;  // keeps sinfo 8-byte aligned
+  static constexpr size_t INFO_BYTES = (size_t)WARPS * TS * 16;
   static constexpr size_t SMEM = 128 + RING_BYTES + YST_BYTES + INFO_BYTES + 2 * NST * 8;
 };
 
@@ -61,12 +68,16 @@ __host__ __device__ constexpr OutTables<MO, RO, MI> make_out_tables() {
   return T;
 }
 
-// select v[i] for a runtime i from a compile-time row (a chain of selects)
+// v[i] for a runtime i from a compile-time row, as a sum of masked products: a
+// select chain gets turned back into an indexed load, which would put the whole
+// constexpr coefficient table in local memory
 template <int N>
 __device__ __forceinline__ float csel(const float (&v)[kMaxL], int i) {
-  float r = v[0];
+  float r = 0.f;
 #pragma unroll
-  for (int k = 1; k < N; ++k) r = (i == k) ? v[k] : r;
+  for (int k = 0; k < N; ++k) {
+    if (v[k] != 0.f) r = fmaf((i == k) ? 1.f : 0.f, v[k], r);
+  }
   return r;
 }
 
@@ -92,13 +103,13 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI>::THREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NST; ++i) {
       ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&empty[i]), C::CO);
+      ptx::mbar_init(ptx::smem_u32(&empty[i]), C::WARPS);
     }
     ptx::mbar_init_fence();
   }
   __syncthreads();
 
-  if (warp == C::CO) {
+  if (warp == C::WARPS) {
     // ------------------------------ TMA producer ------------------------------
     if (lane == 0) {
       ptx::tma_prefetch(&mapM);
@@ -119,53 +130,91 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI>::THREADS, 1)
   }
 
   // -------------------------------- consumers ---------------------------------
+  constexpr int QW = C::QW;
+  const int cw_ = warp / C::SPL, part = warp - cw_ * C::SPL;   // channel within unit, column part
+  const int T0 = part * C::TH;                                  // first outer output of this part
   float* yst = ystage + warp * C::YST;
   long long* info = sinfo + warp * (C::TS * 2);
   const long long HoWo = (long long)g.Ho * g.Wo;
   const int rowstride = (g.mode == 2) ? 2 * g.Wo : g.Wo;
   const int colstride = (g.mode == 2) ? 2 : 1;
+  // split parts: this part's rows of A_o^T (runtime-selected once)
+  float cwo[C::TH][LO];
+#pragma unroll
+  for (int k = 0; k < C::TH; ++k)
+#pragma unroll
+    for (int po = 0; po < LO; ++po) {
+      float c = 0.f;
+#pragma unroll
+      for (int t = 0; t < MO; ++t)
+        if (F.AoT[t][po] != 0.f) c = fmaf((T0 + k == t) ? 1.f : 0.f, F.AoT[t][po], c);
+      cwo[k][po] = c;
+    }
   int st = 0;
   uint32_t ph = 0;
   for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
     const long long t0 = (long long)(u / ngroups) * C::TS;
-    const int coe = (u % ngroups) * C::CO + warp;
+    const int coe = (u % ngroups) * C::CO + cw_;
 
-    float Y[MA][MA];
+    float Y[MA][QW];
 #pragma unroll
     for (int i = 0; i < MA; ++i)
 #pragma unroll
-      for (int j = 0; j < MA; ++j) Y[i][j] = 0.f;
+      for (int j = 0; j < QW; ++j) Y[i][j] = 0.f;
 
 #pragma unroll 1
     for (int p_o = 0; p_o < LO; ++p_o) {
-      float uacc[MI][MA];
+      float uacc[MI][QW];
 #pragma unroll
       for (int s = 0; s < MI; ++s)
 #pragma unroll
-        for (int j = 0; j < MA; ++j) uacc[s][j] = 0.f;
+        for (int j = 0; j < QW; ++j) uacc[s][j] = 0.f;
 #pragma unroll
       for (int p_i = 0; p_i < LI; ++p_i) {
         ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
-        const float* src = ring + st * C::STAGE + warp * C::TS + lane;
-        float mv[PA], qv[MA];
+        const float* src = ring + st * C::STAGE + cw_ * C::TS + lane;
+        float mv[PA], qv[QW];
 #pragma unroll
         for (int p_w = 0; p_w < PA; ++p_w) mv[p_w] = src[p_w * (C::CO * C::TS)];
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[st]));
         if (++st == C::NST) { st = 0; ph ^= 1; }
-        out_axis<MO, RO, MI>(mv, qv);
+        if constexpr (C::SPL == 1) {
+          out_axis<MO, RO, MI>(mv, qv);
+        } else {
+          // inner level on every outer point, then this part's outer rows
+          float uw[LO][MI];
+#pragma unroll
+          for (int po = 0; po < LO; ++po) {
+            float col[LI], o[MI];
+#pragma unroll
+            for (int pi = 0; pi < LI; ++pi) col[pi] = mv[po * LI + pi];
+            K1<MI, kRi>::at(col, o);
+#pragma unroll
+            for (int s2 = 0; s2 < MI; ++s2) uw[po][s2] = o[s2];
+          }
+#pragma unroll
+          for (int k = 0; k < C::TH; ++k)
+#pragma unroll
+            for (int s2 = 0; s2 < MI; ++s2) {
+              float acc = 0.f;
+#pragma unroll
+              for (int po = 0; po < LO; ++po) acc = fmaf(cwo[k][po], uw[po][s2], acc);
+              qv[k * MI + s2] = acc;
+            }
+        }
 #pragma unroll
         for (int s = 0; s < MI; ++s) {
           const float a = F.AiT[s][p_i];
           if (a == 1.f) {
 #pragma unroll
-            for (int j = 0; j < MA; ++j) uacc[s][j] += qv[j];
+            for (int j = 0; j < QW; ++j) uacc[s][j] += qv[j];
           } else if (a == -1.f) {
 #pragma unroll
-            for (int j = 0; j < MA; ++j) uacc[s][j] -= qv[j];
+            for (int j = 0; j < QW; ++j) uacc[s][j] -= qv[j];
           } else if (a != 0.f) {
 #pragma unroll
-            for (int j = 0; j < MA; ++j) uacc[s][j] = fmaf(a, qv[j], uacc[s][j]);
+            for (int j = 0; j < QW; ++j) uacc[s][j] = fmaf(a, qv[j], uacc[s][j]);
           }
         }
       }
@@ -175,7 +224,7 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI>::THREADS, 1)
 #pragma unroll
         for (int s = 0; s < MI; ++s)
 #pragma unroll
-          for (int j = 0; j < MA; ++j) Y[t * MI + s][j] = fmaf(c, uacc[s][j], Y[t * MI + s][j]);
+          for (int j = 0; j < QW; ++j) Y[t * MI + s][j] = fmaf(c, uacc[s][j], Y[t * MI + s][j]);
       }
     }
 
@@ -223,17 +272,19 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI>::THREADS, 1)
 #pragma unroll
     for (int i = 0; i < MA; ++i)
 #pragma unroll
-      for (int j = 0; j < MA; ++j) yst[lane * (MA * MA) + i * MA + j] = Y[i][j];
+      for (int j = 0; j < QW; ++j) yst[lane * (MA * QW) + i * QW + j] = Y[i][j];
     __syncwarp();
     const float slope = (slopes && coe < g.cout_e) ? slopes[g.mode == 2 ? coe % g.Cout : coe] : 0.f;
+    const int qw0 = T0 * MI;  // first output column of this part
 #pragma unroll 1
-    for (int jj = 0; jj < MA; ++jj) {
-      const int e = lane + 32 * jj;  // (slice s, column q_w) pairs, q_w fastest
-      const int s = e / MA, q_w = e - s * MA;
+    for (int jj = 0; jj < QW; ++jj) {
+      const int e = lane + 32 * jj;  // (slice s, local column ql) pairs, ql fastest
+      const int s = e / QW, ql = e - s * QW;
+      const int q_w = qw0 + ql;
       const uint32_t ia = ptx::smem_u32(info) + (uint32_t)s * 16u;
       const long long b = ptx::lds_s64(ia);
       const int lim = (int)ptx::lds_s64(ia + 8);
-      const uint32_t ya = ptx::smem_u32(yst) + (uint32_t)(s * (MA * MA) + q_w) * 4u;
+      const uint32_t ya = ptx::smem_u32(yst) + (uint32_t)(s * (MA * QW) + ql) * 4u;
       const int limh = lim & 255, limw = (lim >> 8) & 255;
       const int khi = (lim >> 16) & 3, kwi = (lim >> 18) & 3;
       const unsigned kh = khi == 0 ? OT.keep[0] : khi == 1 ? OT.keep[1] : OT.keep[2];
@@ -241,12 +292,12 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI>::THREADS, 1)
       int pw = 0;
 #pragma unroll
       for (int q = 0; q < MA; ++q) pw = (q_w == q) ? OT.pos[q] : pw;
-      const bool okw = b >= 0 && ((kw >> q_w) & 1u) && pw < limw;
+      const bool okw = b >= 0 && q_w < MA && ((kw >> q_w) & 1u) && pw < limw;
       YT* dst = y + (b < 0 ? 0 : b) + (long long)pw * colstride;
 #pragma unroll
       for (int q_h = 0; q_h < MA; ++q_h) {
         if (okw && ((kh >> q_h) & 1u) && OT.pos[q_h] < limh) {
-          float v = ptx::lds_f32(ya + q_h * MA * 4);
+          float v = ptx::lds_f32(ya + q_h * QW * 4);
           if (slopes) v = v >= 0.f ? v : slope * v;
           dst[(long long)OT.pos[q_h] * rowstride] = from_f<YT>(v);
         }
@@ -273,7 +324,7 @@ static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const f
   const uint32_t box[3] = {(uint32_t)C::TS, (uint32_t)C::CO, (uint32_t)X::PA};
   if (!encode_tmap(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, M, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
     return NW_ERR_CUDA;
-  const int ngroups = g.cout_pad / C::CO;
+  const int ngroups = (g.cout_pad + C::CO - 1) / C::CO;
   const long long tchunks = (g.T + C::TS - 1) / C::TS;
   const long long nunits = tchunks * ngroups;
   int sms = 148, dev = 0;

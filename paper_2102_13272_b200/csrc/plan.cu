@@ -361,7 +361,7 @@ nw_status_t nw_workspace_size(nw_plan_t p, int N, int H, int W, size_t *bytes) {
   if (st != NW_OK) return st;
   Geometry g = make_geometry(p, N, H, W);
   if (g.Ho < 1 || g.Wo < 1) return NW_ERR_INVALID;
-  *bytes = v_bytes(p, g) + m_bytes(p, g);
+  *bytes = forward_ws_bytes(p, N, H, W);
   return NW_OK;
 }
 

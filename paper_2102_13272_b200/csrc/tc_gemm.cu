@@ -320,6 +320,7 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long units = (long long)prm.P * prm.ngrp;
+  if (g.gemm_ctas > 0 && g.gemm_ctas < sms) sms = g.gemm_ctas;
   const int grid = (int)(units < sms ? units : sms);
   LaunchScope scope_("contraction_tc", s);
   tc::contraction_kernel<<<grid, tc::kThreads, smem, s>>>(mapV, mapU, prm);

@@ -7,9 +7,9 @@
 // per axis in the factored two-level form (B_o^T (x) B_i^T: inner F(m_i,3) on each
 // reordered column, then outer F(m_o,r_o) across columns).  Each level is one
 // 1-D kernel (K1<m,r>::bt / ::at): generic kernels skip zero and +-1 coefficients at
-// compile time; F(3,3) -- the kernel at both levels of the default plan -- has
-// hand-factored forms with shared subexpressions (9 instead of 18 operations
-// for B^T, 7 instead of 11 for A^T).  Float addition is not associative, so the
+// compile time; F(3,3) -- the kernel at both levels of the default plan -- and
+// F(4,3) have hand-factored forms with shared subexpressions (F(3,3): 9 instead
+// of 18 operations for B^T, 7 instead of 11 for A^T; F(4,3): 12 and 10).  Float addition is not associative, so the
 // compiler cannot find these factorizations itself; the rounding order differs
 // from the plain matrix product by a few ulp, far inside the accuracy budget.
 #pragma once
@@ -89,6 +89,32 @@ struct K1<3, 3> {
     o[0] = (x[0] + x[3]) + s;                            // x0 + x1 + x2 + x3
     o[1] = fmaf(2.f, x[3], d);                           // x1 - x2 + 2x3
     o[2] = fmaf(4.f, x[3], s) + x[4];                    // x1 + x2 + 4x3 + x4
+  }
+};
+
+// F(4,3), points {0, 1, -1, 2, -2, inf}:
+//   B^T = [4 0 -5 0 1 0; 0 4 4 -1 -1 0; 0 -4 4 1 -1 0; 0 -2 -1 2 1 0; 0 2 -1 -2 1 0; 0 4 0 -5 0 1]
+//   A^T = [1 1 1 1 1 0; 0 1 -1 2 -2 0; 0 1 1 4 4 0; 0 1 -1 8 -8 1]
+template <>
+struct K1<4, 3> {
+  static constexpr int L = 6;
+  __device__ __forceinline__ static void bt(const float (&x)[6], float (&o)[6]) {
+    const float a = fmaf(-4.f, x[2], x[4]);              // x4 - 4x2
+    const float b = fmaf(-4.f, x[1], x[3]);              // x3 - 4x1
+    const float c = x[4] - x[2], d = x[3] - x[1];
+    o[0] = fmaf(4.f, x[0], fmaf(-5.f, x[2], x[4]));      // 4x0 - 5x2 + x4
+    o[1] = -a - b;                                       // 4x1 + 4x2 - x3 - x4
+    o[2] = b - a;                                        // -4x1 + 4x2 + x3 - x4
+    o[3] = fmaf(2.f, d, c);                              // -2x1 - x2 + 2x3 + x4
+    o[4] = fmaf(-2.f, d, c);                             // 2x1 - x2 - 2x3 + x4
+    o[5] = fmaf(4.f, x[1], fmaf(-5.f, x[3], x[5]));      // 4x1 - 5x3 + x5
+  }
+  __device__ __forceinline__ static void at(const float (&x)[6], float (&o)[4]) {
+    const float s1 = x[1] + x[2], d1 = x[1] - x[2], s2 = x[3] + x[4], d2 = x[3] - x[4];
+    o[0] = (x[0] + s1) + s2;                             // x0 + x1 + x2 + x3 + x4
+    o[1] = fmaf(2.f, d2, d1);                            // x1 - x2 + 2x3 - 2x4
+    o[2] = fmaf(4.f, s2, s1);                            // x1 + x2 + 4x3 + 4x4
+    o[3] = fmaf(8.f, d2, d1) + x[5];                     // x1 - x2 + 8x3 - 8x4 + x5
   }
 };
 

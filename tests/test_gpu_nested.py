@@ -127,3 +127,15 @@ def test_edge_shapes_bf16x3(N, H, W):
     layer = synth.small(synth.CONFIGS["c2k9"], N=N, H=H, W=W, Cin=16, Cout=32)
     t, y = _run(layer, "bf16x3")
     assert rel_err(y, _ref(layer, t)) <= TOL["bf16x3"]
+
+
+@pytest.mark.parametrize("m_o", [3, 4, 5])
+@pytest.mark.parametrize("name", ["c2k5", "c2k7", "c2k9", "c3", "c4b", "c5_deconv"])
+@pytest.mark.parametrize("math", ["fp32", "bf16x3"])
+def test_larger_outer_tile(m_o, name, math):
+    # F(m_o,3) (x) F(3,3): (3 m_o) x (3 m_o) outputs per slice; same gates
+    layer = SMALL[name].with_(m_o=m_o)
+    t, y = _run(layer, math)
+    ref = _ref(layer, t)
+    tol = TOL[math] if layer.dtype == "f32" else max(TOL[math], 2.0 ** -8)
+    assert rel_err(y, ref) <= tol

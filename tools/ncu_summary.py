@@ -8,7 +8,9 @@ Writes profiles/<tag>_launches.csv (per-kernel share of the launch list),
 profiles/<tag>_ncu.md (key --set full metrics per captured kernel) and, when
 --bench is given, copies the bench JSON line to profiles/<tag>_bench.json.
 Also updates profiles/traffic.json with dram read+write bytes per launch,
-keyed "<kind>:<math>", which bench.py reports as roofline.traffic.
+keyed "<kind>:<math>:<layer>:m<m_outer>" (the layer tools/prof_layer.py ran; the
+report file name carries it: prof_<tag>_<layer>_<kernel>.ncu-rep), which
+bench.py averages over the workload's layers as roofline.traffic.
 """
 from __future__ import annotations
 
@@ -103,6 +105,7 @@ def main():
     ap.add_argument("--rep", nargs="*", default=[])
     ap.add_argument("--bench")
     ap.add_argument("--math", default="bf16x3")
+    ap.add_argument("--m-outer", type=int, default=4, help="outer kernel of the profiled plan")
     ap.add_argument("--note", default="")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
@@ -127,9 +130,10 @@ def main():
             md.append("")
             if "dram__bytes_read.sum" in d and "dram__bytes_write.sum" in d:
                 b = to_bytes(*d["dram__bytes_read.sum"]) + to_bytes(*d["dram__bytes_write.sum"])
+                layer = os.path.basename(rep).split("_")[2] if os.path.basename(rep).count("_") >= 3 else "?"
                 for key, kind in KIND.items():
                     if key in d["kernel"]:
-                        traffic[f"{kind}:{a.math}"] = int(b)
+                        traffic[f"{kind}:{a.math}:{layer}:m{a.m_outer}"] = int(b)
     json.dump(traffic, open(tfile, "w"), indent=1, sort_keys=True)
     if a.bench:
         line = [l for l in open(a.bench).read().splitlines() if l.startswith("{")][-1]
