@@ -8,6 +8,8 @@ template <int MO, int RO, int MI>
 nw_status_t input_impl(const nw_plan_st*, const Geometry&, const void*, void*, cudaStream_t);
 template <int MO, int RO, int MI>
 nw_status_t output_impl(const nw_plan_st*, const Geometry&, const float*, void*, cudaStream_t);
+template <int MO, int RO, int MI>
+nw_status_t output_impl_pre(const nw_plan_st*, const Geometry&, const float*, void*, cudaStream_t);
 
 #define NW_DISPATCH_AXIS(p, FN, ...)                                       \
   do {                                                                     \
@@ -28,6 +30,11 @@ nw_status_t launch_input_transform(const nw_plan_st* p, const Geometry& g, const
 
 nw_status_t launch_output_transform(const nw_plan_st* p, const Geometry& g, const float* M, void* y, cudaStream_t s) {
   NW_DISPATCH_AXIS(p, output_impl, p, g, M, y, s);
+}
+
+nw_status_t launch_output_transform_pre(const nw_plan_st* p, const Geometry& g, const float* M, void* y,
+                                        cudaStream_t s) {
+  NW_DISPATCH_AXIS(p, output_impl_pre, p, g, M, y, s);
 }
 
 }  // namespace nw

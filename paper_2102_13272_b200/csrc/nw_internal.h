@@ -95,6 +95,12 @@ nw_status_t launch_output_transform(const nw_plan_st *p, const Geometry &g, cons
 nw_status_t launch_gemm_simt(const nw_plan_st *p, const Geometry &g, const float *V, const float *U,
                              float *M, cudaStream_t s);
 // tcgen05 contraction (tc_gemm.cu)
+bool gemm_fused_eligible(const nw_plan_st *p, const Geometry &g);
+nw_status_t launch_gemm_tc_fused(const nw_plan_st *p, const Geometry &g, const void *V, const void *U, float *Mp,
+                                 cudaStream_t s);
+// output transform of a fused contraction: M holds M' (inner w level applied)
+nw_status_t launch_output_transform_pre(const nw_plan_st *p, const Geometry &g, const float *Mp, void *y,
+                                        cudaStream_t s);
 nw_status_t launch_gemm_tc(const nw_plan_st *p, const Geometry &g, const void *V, const void *U,
                            float *M, cudaStream_t s);
 

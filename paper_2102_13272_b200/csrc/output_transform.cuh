@@ -23,20 +23,27 @@
 
 namespace nw {
 
-template <int MO, int RO, int MI>
+template <int MO, int RO, int MI, bool PRE = false>
 struct OutCfg {
   using X = Ax<MO, RO, MI>;
+  // PRE: M already carries the inner output level along w (fused contraction
+  // epilogue), so a point row holds l_o * m_i values instead of P_a
+  static constexpr int RL = PRE ? X::LO * MI : X::PA;
   // Threads keep (part of) the M_a x M_a output tile in registers.  Up to 9 x 9
   // one thread owns the tile (SPL = 1); larger outer kernels split the output
   // columns by outer index t into SPL parts of TH outer outputs each.
   static constexpr int SPL = (X::MA <= 9) ? 1 : (MO <= 4 ? 2 : 3);
   static constexpr int TH = (MO + SPL - 1) / SPL;   // outer outputs per part
   static constexpr int QW = (SPL == 1) ? X::MA : TH * MI;  // output columns per thread
-  static constexpr int CO = (SPL == 1) ? 8 : (SPL == 2 ? 4 : 3);  // output channels per unit
+  // output channels per unit.  Registers are split per SM sub-partition (16K each, warps
+  // dealt round-robin): 9 warps allow 168 registers per thread, 13 allow 128.  The
+  // kernel is latency-bound, so pre-reduced rows (18 instead of 30 values) buy 12
+  // consumer warps for the split 12 x 12 tile.
+  static constexpr int CO = (SPL == 1) ? 8 : (SPL == 2 ? (PRE ? 6 : 4) : 3);
   static constexpr int WARPS = CO * SPL;          // consumer warps
   static constexpr int TS = 32;  // slices per unit (lanes)
   static constexpr int NST = 4;  // ring depth (point rows)
-  static constexpr int STAGE = X::PA * CO * TS;     // floats per ring stage
+  static constexpr int STAGE = RL * CO * TS;        // floats per ring stage
   static constexpr int YST = TS * X::MA * QW + 1;   // floats per warp output stage
   static constexpr int THREADS = (WARPS + 1) * 32;
   static constexpr size_t RING_BYTES = (size_t)NST * STAGE * 4;
@@ -81,12 +88,13 @@ __device__ __forceinline__ float csel(const float (&v)[kMaxL], int i) {
   return r;
 }
 
-template <int MO, int RO, int MI, typename YT>
-__global__ void __launch_bounds__(OutCfg<MO, RO, MI>::THREADS, 1)
+template <int MO, int RO, int MI, typename YT, bool PRE>
+__global__ void __launch_bounds__(OutCfg<MO, RO, MI, PRE>::THREADS, 1)
     output_transform_kernel(const __grid_constant__ CUtensorMap mapM, YT* __restrict__ y, Geometry g,
                             const float* __restrict__ slopes, int nunits, int ngroups) {
   using X = Ax<MO, RO, MI>;
-  using C = OutCfg<MO, RO, MI>;
+  using C = OutCfg<MO, RO, MI, PRE>;
+  constexpr int RL = C::RL;
   constexpr AxisF F = axis_f(MO, RO, MI);
   constexpr OutTables<MO, RO, MI> OT = make_out_tables<MO, RO, MI>();
   constexpr int MA = X::MA, PA = X::PA, LO = X::LO, LI = X::LI, NPH = X::NPH;
@@ -121,7 +129,7 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI>::THREADS, 1)
           ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
           const uint32_t fb = ptx::smem_u32(&full[st]);
           ptx::mbar_expect_tx(fb, C::STAGE * 4);
-          ptx::tma_load_3d(ptx::smem_u32(ring + st * C::STAGE), &mapM, fb, t0, co0, r * PA);
+          ptx::tma_load_3d(ptx::smem_u32(ring + st * C::STAGE), &mapM, fb, t0, co0, r * RL);
           if (++st == C::NST) { st = 0; ph ^= 1; }
         }
       }
@@ -173,19 +181,20 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI>::THREADS, 1)
       for (int p_i = 0; p_i < LI; ++p_i) {
         ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
         const float* src = ring + st * C::STAGE + cw_ * C::TS + lane;
-        float mv[PA], qv[QW];
+        float mv[RL], qv[QW];
 #pragma unroll
-        for (int p_w = 0; p_w < PA; ++p_w) mv[p_w] = src[p_w * (C::CO * C::TS)];
+        for (int p_w = 0; p_w < RL; ++p_w) mv[p_w] = src[p_w * (C::CO * C::TS)];
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[st]));
         if (++st == C::NST) { st = 0; ph ^= 1; }
-        if constexpr (C::SPL == 1) {
-          out_axis<MO, RO, MI>(mv, qv);
-        } else {
-          // inner level on every outer point, then this part's outer rows
-          float uw[LO][MI];
+        // inner level along w on every outer point (done by the contraction epilogue when PRE)
+        float uw[LO][MI];
 #pragma unroll
-          for (int po = 0; po < LO; ++po) {
+        for (int po = 0; po < LO; ++po) {
+          if constexpr (PRE) {
+#pragma unroll
+            for (int s2 = 0; s2 < MI; ++s2) uw[po][s2] = mv[po * MI + s2];
+          } else {
             float col[LI], o[MI];
 #pragma unroll
             for (int pi = 0; pi < LI; ++pi) col[pi] = mv[po * LI + pi];
@@ -193,6 +202,20 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI>::THREADS, 1)
 #pragma unroll
             for (int s2 = 0; s2 < MI; ++s2) uw[po][s2] = o[s2];
           }
+        }
+        if constexpr (C::SPL == 1) {
+          // outer level, all outputs
+#pragma unroll
+          for (int s2 = 0; s2 < MI; ++s2) {
+            float col[LO], o[MO];
+#pragma unroll
+            for (int po = 0; po < LO; ++po) col[po] = uw[po][s2];
+            K1<MO, RO>::at(col, o);
+#pragma unroll
+            for (int t = 0; t < MO; ++t) qv[t * MI + s2] = o[t];
+          }
+        } else {
+          // this part's outer rows
 #pragma unroll
           for (int k = 0; k < C::TH; ++k)
 #pragma unroll
@@ -307,11 +330,11 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI>::THREADS, 1)
   }
 }
 
-template <int MO, int RO, int MI, typename YT>
+template <int MO, int RO, int MI, typename YT, bool PRE>
 static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const float* M, void* y, cudaStream_t s) {
-  using C = OutCfg<MO, RO, MI>;
+  using C = OutCfg<MO, RO, MI, PRE>;
   using X = Ax<MO, RO, MI>;
-  auto kern = output_transform_kernel<MO, RO, MI, YT>;
+  auto kern = output_transform_kernel<MO, RO, MI, YT, PRE>;
   static bool attr_done = false;
   if (!attr_done) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
@@ -319,9 +342,10 @@ static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const f
     attr_done = true;
   }
   alignas(64) CUtensorMap map;
-  const uint64_t dims[3] = {(uint64_t)g.T_pad, (uint64_t)g.cout_pad, (uint64_t)g.P};
+  const uint64_t rows = PRE ? (uint64_t)X::PA * C::RL : (uint64_t)g.P;
+  const uint64_t dims[3] = {(uint64_t)g.T_pad, (uint64_t)g.cout_pad, rows};
   const uint64_t strides[2] = {(uint64_t)g.T_pad * 4, (uint64_t)g.T_pad * g.cout_pad * 4};
-  const uint32_t box[3] = {(uint32_t)C::TS, (uint32_t)C::CO, (uint32_t)X::PA};
+  const uint32_t box[3] = {(uint32_t)C::TS, (uint32_t)C::CO, (uint32_t)C::RL};
   if (!encode_tmap(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, M, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
     return NW_ERR_CUDA;
   const int ngroups = (g.cout_pad + C::CO - 1) / C::CO;
@@ -338,8 +362,16 @@ static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const f
 
 template <int MO, int RO, int MI>
 nw_status_t output_impl(const nw_plan_st* p, const Geometry& g, const float* M, void* y, cudaStream_t s) {
-  if (p->dtype == NW_DTYPE_BF16) return output_launch<MO, RO, MI, __nv_bfloat16>(p, g, M, y, s);
-  return output_launch<MO, RO, MI, float>(p, g, M, y, s);
+  if (p->dtype == NW_DTYPE_BF16) return output_launch<MO, RO, MI, __nv_bfloat16, false>(p, g, M, y, s);
+  return output_launch<MO, RO, MI, float, false>(p, g, M, y, s);
+}
+template <int MO, int RO, int MI>
+nw_status_t output_impl_pre(const nw_plan_st* p, const Geometry& g, const float* M, void* y, cudaStream_t s) {
+  if constexpr (MI == 3) {
+    if (p->dtype == NW_DTYPE_BF16) return output_launch<MO, RO, MI, __nv_bfloat16, true>(p, g, M, y, s);
+    return output_launch<MO, RO, MI, float, true>(p, g, M, y, s);
+  }
+  return NW_ERR_UNSUPPORTED;
 }
 
 }  // namespace nw

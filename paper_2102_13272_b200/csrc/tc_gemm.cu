@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "nw_internal.h"
@@ -256,6 +257,176 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u));
 }
 
+
+// ---------------------------------------------------------------------------
+// Contraction with the inner level of the output transform fused into the
+// epilogue (Y = A^T_hat M A_hat, A^T_hat = A_o^T (x) A_i^T).  A unit is
+// the l_i consecutive points (p_h, p_o, p_i = 0 .. l_i-1) of one 128-slice
+// block; their accumulators land in a ring of NSLOT TMEM slots (N columns each),
+// and 8 epilogue warps (two per TMEM lane quarter, one column half each) fold
+// each slot into m_i partial sums with the compile-time A_i^T as soon as it is
+// committed, so only M' = (A_i^T along w) M -- m_i/l_i of M -- reaches HBM:
+//   M'[((p_h * l_o + p_o) * m_i + s)][co][t] = sum_{p_i} A_i^T[s][p_i] M[(p_h, p_o, p_i)][co][t]
+// ---------------------------------------------------------------------------
+constexpr int kFuseThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+constexpr int kSlots = 8;
+
+struct FusedParams {
+  int nmb, N, KB, lo, nst;
+  int PA, LO;             // points per axis, outer points per axis
+  long long T_pad;
+  long long a_lo_row, b_lo_row;
+  float* Mp;
+};
+
+template <int MI>
+__global__ void __launch_bounds__(kFuseThreads, 1)
+    contraction_fused_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapU,
+                             const FusedParams p) {
+  constexpr int LI = MI + 2;
+  constexpr Kernel1D KI = make_kernel(MI, 3);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* sbase = smem_raw + (base - raw);
+  const uint32_t a_plane = kBM * kBK * 2, b_plane = (uint32_t)p.N * kBK * 2;
+  const uint32_t a_bytes = a_plane * (p.lo ? 2 : 1), b_bytes = b_plane * (p.lo ? 2 : 1);
+  const uint32_t stage = a_bytes + b_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + (size_t)stage * p.nst);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kMaxStages;
+  uint64_t* s_full = bars + 2 * kMaxStages;
+  uint64_t* s_empty = bars + 2 * kMaxStages + kSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 2 * kSlots);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int units = p.nmb * p.PA * p.LO;
+  const uint32_t tcols = (uint32_t)(kSlots * p.N) <= 32 ? 32u : (uint32_t)(kSlots * p.N);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapV);
+    tma_prefetch(&mapU);
+    for (int i = 0; i < p.nst; ++i) { mbar_init(smem_u32(&full[i]), 1); mbar_init(smem_u32(&empty[i]), 1); }
+    for (int i = 0; i < kSlots; ++i) { mbar_init(smem_u32(&s_full[i]), 1); mbar_init(smem_u32(&s_empty[i]), 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(tcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------- TMA producer -------------------------
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int pg = u / p.nmb, mb = u - pg * p.nmb;
+        const int p_h = pg / p.LO, p_o = pg - p_h * p.LO;
+        for (int pi = 0; pi < LI; ++pi) {
+          const int xi = p_h * p.PA + p_o * LI + pi;
+          for (int kb = 0; kb < p.KB; ++kb) {
+            mbar_wait(smem_u32(&empty[st]), ph ^ 1);
+            const uint32_t fb = smem_u32(&full[st]);
+            mbar_expect_tx(fb, stage);
+            const uint32_t dst = base + (uint32_t)st * stage;
+            const long long row = (long long)xi * p.T_pad + (long long)mb * kBM;
+            tma_load_2d(dst, &mapV, fb, kb * kBK, (int)row);
+            if (p.lo) tma_load_2d(dst + a_plane, &mapV, fb, kb * kBK, (int)(p.a_lo_row + row));
+            tma_load_2d(dst + a_bytes, &mapU, fb, kb * kBK, xi * p.N);
+            if (p.lo) tma_load_2d(dst + a_bytes + b_plane, &mapU, fb, kb * kBK, (int)(p.b_lo_row + (long long)xi * p.N));
+            if (++st == p.nst) { st = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------- MMA issuer ---------------------------
+      const uint32_t idesc = idesc_bf16(p.N);
+      int st = 0;
+      uint32_t ph = 0;
+      uint32_t sc = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        for (int pi = 0; pi < LI; ++pi, ++sc) {
+          const uint32_t slot = sc % kSlots, spar = (sc / kSlots) & 1;
+          mbar_wait(smem_u32(&s_empty[slot]), spar ^ 1);
+          fence_after();
+          const uint32_t acc = tmem_base + slot * (uint32_t)p.N;
+          for (int kb = 0; kb < p.KB; ++kb) {
+            mbar_wait(smem_u32(&full[st]), ph);
+            fence_after();
+            const uint32_t asm_ = base + (uint32_t)st * stage, bsm = asm_ + a_bytes;
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t ah = sw128_desc(asm_ + k * 32), bh = sw128_desc(bsm + k * 32);
+              umma_f16(acc, ah, bh, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              if (p.lo) {
+                umma_f16(acc, ah, sw128_desc(bsm + b_plane + k * 32), idesc, 1u);
+                umma_f16(acc, sw128_desc(asm_ + a_plane + k * 32), bh, idesc, 1u);
+              }
+            }
+            umma_commit(smem_u32(&empty[st]));
+            if (++st == p.nst) { st = 0; ph ^= 1; }
+          }
+          umma_commit(smem_u32(&s_full[slot]));
+        }
+      }
+    }
+  } else {  // ------------------------------- epilogue ----------------------------------
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int NH = p.N >> 1;               // 16 or 32 columns per warp
+    uint32_t sc = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int pg = u / p.nmb, mb = u - pg * p.nmb;
+      float out[MI][32];
+#pragma unroll
+      for (int s = 0; s < MI; ++s)
+#pragma unroll
+        for (int c = 0; c < 32; ++c) out[s][c] = 0.f;
+#pragma unroll
+      for (int pi = 0; pi < LI; ++pi, ++sc) {
+        const uint32_t slot = sc % kSlots, spar = (sc / kSlots) & 1;
+        mbar_wait(smem_u32(&s_full[slot]), spar);
+        fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * (uint32_t)p.N + (uint32_t)(half * NH);
+        uint32_t r0[16], r1[16];
+        tmem_ld16(taddr, r0);
+        if (NH == 32) tmem_ld16(taddr + 16, r1);
+        tmem_ld_wait();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&s_empty[slot]));
+#pragma unroll
+        for (int s = 0; s < MI; ++s) {
+          const float a = float(rdouble(KI.AT[s][pi]));
+          if (a == 0.f) continue;
+#pragma unroll
+          for (int c = 0; c < 16; ++c) out[s][c] = fmaf(a, __uint_as_float(r0[c]), out[s][c]);
+          if (NH == 32) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) out[s][16 + c] = fmaf(a, __uint_as_float(r1[c]), out[s][16 + c]);
+          }
+        }
+      }
+      const long long t = (long long)mb * kBM + q * 32 + lane;
+#pragma unroll
+      for (int s = 0; s < MI; ++s) {
+        float* dst = p.Mp + ((long long)(pg * MI + s) * p.N + half * NH) * p.T_pad + t;
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          if (c < NH) dst[(long long)c * p.T_pad] = out[s][c];
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tcols));
+}
+
 }  // namespace tc
 
 // ------------------------------ host side ------------------------------------
@@ -324,6 +495,59 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   const int grid = (int)(units < sms ? units : sms);
   LaunchScope scope_("contraction_tc", s);
   tc::contraction_kernel<<<grid, tc::kThreads, smem, s>>>(mapV, mapU, prm);
+  return check_launch();
+}
+
+// Fused contraction + inner output level (see contraction_fused_kernel).  Eligible
+// for the nested path in the tensor-core modes with Cout_pad in {32, 64} and
+// inner F(3,3); M' ([P_a * l_o * m_i][cout_pad][T_pad]) is written to M.
+bool gemm_fused_eligible(const nw_plan_st* p, const Geometry& g) {
+  static const int on = [] {
+    const char* v = getenv("NW_FUSE_AI");
+    return v ? atoi(v) : 1;
+  }();
+  return on && g.path == kPathNested && p->math != NW_MATH_FP32_SIMT && (g.cout_pad == 32 || g.cout_pad == 64) &&
+         g.mi == 3 && g.nsh == 1;
+}
+
+nw_status_t launch_gemm_tc_fused(const nw_plan_st* p, const Geometry& g, const void* V, const void* U, float* Mp,
+                                 cudaStream_t s) {
+  tc::FusedParams prm{};
+  prm.nmb = (int)(g.T_pad / tc::kBM);
+  prm.N = g.cout_pad;
+  prm.KB = (g.cin_pad + tc::kBK - 1) / tc::kBK;
+  prm.lo = (p->math == NW_MATH_BF16X3) ? 1 : 0;
+  const NestedAxis ax = path_axis(p, g.path);
+  prm.PA = ax.Pa;
+  prm.LO = ax.l_o;
+  prm.T_pad = g.T_pad;
+  prm.a_lo_row = (long long)g.P * g.T_pad;
+  prm.b_lo_row = (long long)g.P * g.cout_pad;
+  prm.Mp = Mp;
+  const uint32_t stage = (tc::kBM * tc::kBK * 2 + (uint32_t)prm.N * tc::kBK * 2) * (prm.lo ? 2 : 1);
+  prm.nst = (int)((200u * 1024u) / stage);
+  if (prm.nst > tc::kMaxStages) prm.nst = tc::kMaxStages;
+  if (prm.nst < 2) return NW_ERR_UNSUPPORTED;
+  const size_t smem = 1024 + (size_t)stage * prm.nst + (2 * tc::kMaxStages + 2 * tc::kSlots + 2) * 8;
+  const long long rowsV = (long long)g.P * g.T_pad * (prm.lo ? 2 : 1);
+  const long long rowsU = (long long)g.P * g.cout_pad * (prm.lo ? 2 : 1);
+  if (rowsV >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
+  alignas(64) CUtensorMap mapV, mapU;
+  if (!make_map(&mapV, V, rowsV, g.cin_pad, tc::kBM)) return NW_ERR_CUDA;
+  if (!make_map(&mapU, U, rowsU, g.cin_pad, prm.N)) return NW_ERR_CUDA;
+  auto kern = tc::contraction_fused_kernel<3>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+      return NW_ERR_CUDA;
+    attr = true;
+  }
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long units = (long long)prm.nmb * prm.PA * prm.LO;
+  const int grid = (int)(units < sms ? units : sms);
+  LaunchScope scope_("contraction_tc", s);
+  kern<<<grid, tc::kFuseThreads, smem, s>>>(mapV, mapU, prm);
   return check_launch();
 }
 
