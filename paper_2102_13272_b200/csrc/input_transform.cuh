@@ -76,7 +76,31 @@ __device__ __forceinline__ void store_row(const float (*za)[Ax<MO, RO, MI>::LI],
   }
 }
 
-template <int MO, int RO, int MI, int SR, int CC, typename XT, bool BF>
+// Same, for the blocked split layout with a compile-time channel pitch CINP:
+// V bytes [T_pad/128][P][2 planes][128 slices][CINP] bf16, so every store of a
+// row is the one base pointer plus an immediate (point * 512 * CINP, plane * 256 * CINP).
+template <int MO, int RO, int MI, int CINP>
+__device__ __forceinline__ void store_row_imm(const float (*za)[Ax<MO, RO, MI>::LI],
+                                              const float (*zb)[Ax<MO, RO, MI>::LI], char* hp) {
+  using X = Ax<MO, RO, MI>;
+  constexpr long long PS = 2ll * 128 * CINP * 2, PL = 128ll * CINP * 2;
+#pragma unroll
+  for (int pi = 0; pi < X::LI; ++pi) {
+    float oa[X::LO], ob[X::LO];
+    in_axis_outer_col<MO, RO, MI>(za, pi, oa);
+    in_axis_outer_col<MO, RO, MI>(zb, pi, ob);
+#pragma unroll
+    for (int po = 0; po < X::LO; ++po) {
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(oa[po], ob[po]);
+      const float2 hf = __bfloat1622float2(hi);
+      char* h = hp + (po * X::LI + pi) * PS;
+      *reinterpret_cast<__nv_bfloat162*>(h) = hi;
+      *reinterpret_cast<__nv_bfloat162*>(h + PL) = __floats2bfloat162_rn(oa[po] - hf.x, ob[po] - hf.y);
+    }
+  }
+}
+
+template <int MO, int RO, int MI, int SR, int CC, typename XT, bool BF, int CINP>
 __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, RO, MI, SR, CC>::MINB)
     input_transform_kernel(const XT* __restrict__ x, void* __restrict__ Vout,
                                                                  Geometry g, int cgroups, int wgroups) {
@@ -175,17 +199,28 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
       in_axis_inner<MO, RO, MI>(bb, zb);
     }
     const long long t = ((((long long)n * g.tiles_h + ah) * g.tiles_w + aw) * NPH + phh) * NPH + pw;
-    const long long o = ((long long)(p_h * PA) * g.T_pad + t) * g.cin_pad + ce;
     constexpr int ES = BF ? 2 : 4;
-    char* hp = reinterpret_cast<char*>(Vout) + o * ES;
-    store_row<MO, RO, MI, BF>(za, zb, hp, hp + plane * ES, pstride * ES);
+    if (BF && g.vblk) {
+      // blocked split layout [T_pad/128][P][hi, lo][128][cin_pad]
+      const long long o = ((((t >> 7) * g.P + (long long)p_h * PA) * 2) * 128 + (t & 127)) * g.cin_pad + ce;
+      char* hp = reinterpret_cast<char*>(Vout) + o * 2;
+      if constexpr (CINP > 0 && BF) {
+        store_row_imm<MO, RO, MI, CINP>(za, zb, hp);
+      } else {
+        store_row<MO, RO, MI, BF>(za, zb, hp, hp + 256ll * g.cin_pad, 512ll * g.cin_pad);
+      }
+    } else {
+      const long long o = ((long long)(p_h * PA) * g.T_pad + t) * g.cin_pad + ce;
+      char* hp = reinterpret_cast<char*>(Vout) + o * ES;
+      store_row<MO, RO, MI, BF>(za, zb, hp, hp + plane * ES, pstride * ES);
+    }
   }
 }
 
-template <int MO, int RO, int MI, int SR, int CC, typename XT, bool BF>
-static nw_status_t input_launch(const Geometry& g, const void* x, void* V, cudaStream_t s) {
+template <int MO, int RO, int MI, int SR, int CC, typename XT, bool BF, int CINP>
+static nw_status_t input_launch_c(const Geometry& g, const void* x, void* V, cudaStream_t s) {
   using C = InCfg<MO, RO, MI, SR, CC>;
-  auto kern = input_transform_kernel<MO, RO, MI, SR, CC, XT, BF>;
+  auto kern = input_transform_kernel<MO, RO, MI, SR, CC, XT, BF, CINP>;
   static bool attr_done = false;  // per instantiation
   if (!attr_done) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
@@ -200,6 +235,16 @@ static nw_status_t input_launch(const Geometry& g, const void* x, void* V, cudaS
   LaunchScope scope_("input_transform", s);
   kern<<<(unsigned)nb, C::THREADS, C::SMEM, s>>>(static_cast<const XT*>(x), V, g, cgroups, wgroups);
   return check_launch();
+}
+
+// compile-time channel pitch for the common blocked layouts (immediate store offsets)
+template <int MO, int RO, int MI, int SR, int CC, typename XT, bool BF>
+static nw_status_t input_launch(const Geometry& g, const void* x, void* V, cudaStream_t s) {
+  if constexpr (BF && SR == 1) {
+    if (g.vblk && g.cin_pad == 64) return input_launch_c<MO, RO, MI, SR, CC, XT, BF, 64>(g, x, V, s);
+    if (g.vblk && g.cin_pad == 256) return input_launch_c<MO, RO, MI, SR, CC, XT, BF, 256>(g, x, V, s);
+  }
+  return input_launch_c<MO, RO, MI, SR, CC, XT, BF, 0>(g, x, V, s);
 }
 
 template <int MO, int RO, int MI, int SR, typename XT, bool BF>

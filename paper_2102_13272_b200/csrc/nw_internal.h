@@ -41,6 +41,7 @@ struct Geometry {
   int nb;            // filter blocks per axis: 1 nested, ceil(Kp/3) OLA (Eq. 2.3), Kp direct (Eq. 2.1 taps)
   int nsh;           // nb^2: contraction K = nsh * cin_pad, A rows shifted per block
   int gemm_ctas;     // persistent contraction grid (0: one CTA per SM)
+  int vblk;          // V in the blocked split layout [T_pad/128][P][hi, lo][128][cin_pad] (nested, bf16x3)
 };
 
 constexpr int kPathNested = 0, kPathOla = 1, kPathDirect = 2;

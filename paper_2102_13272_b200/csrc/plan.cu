@@ -153,6 +153,7 @@ Geometry make_geometry(const nw_plan_st *p, int N, int H, int W, int path) {
   g.cin_pad = p->cin_pad; g.cout_pad = p->cout_pad;
   g.Pa = ax.Pa;
   g.P = g.Pa * g.Pa;
+  g.vblk = (path == kPathNested && p->math == NW_MATH_BF16X3) ? 1 : 0;
   return g;
 }
 

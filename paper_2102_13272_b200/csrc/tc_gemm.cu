@@ -90,6 +90,7 @@ struct Params {
   long long T_pad;
   long long a_lo_row; // row offset of the lo plane in the V tensor map (= P * T_pad)
   long long b_lo_row; // row offset of the lo plane in the U tensor map (= P * N)
+  int vblk;           // blocked split layout: rows ((mb * P + xi) * 2 + plane) * 128
   float* M;
   // shifted operands (OLA / direct comparison paths): k-block kb belongs to
   // shift s = kb / kbc and channel block kc = kb % kbc; its A rows are read at
@@ -169,9 +170,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t afull = smem_u32(&A_full[sa]);
             mbar_expect_tx(afull, a_stage);
             const uint32_t adst = base + a_off + sa * a_stage;
-            const long long row = (long long)xi * p.T_pad + (long long)(mb0 + g) * kBM + aoff;
+            long long row, lrow;
+            if (p.vblk) {
+              row = ((long long)(mb0 + g) * p.P + xi) * (2 * kBM);
+              lrow = row + kBM;
+            } else {
+              row = (long long)xi * p.T_pad + (long long)(mb0 + g) * kBM + aoff;
+              lrow = p.a_lo_row + row;
+            }
             tma_load_2d(adst, &mapV, afull, acol, (int)row);
-            if (p.lo) tma_load_2d(adst + a_plane, &mapV, afull, acol, (int)(p.a_lo_row + row));
+            if (p.lo) tma_load_2d(adst + a_plane, &mapV, afull, acol, (int)lrow);
             if (++sa == p.nA) { sa = 0; pa ^= 1; }
           }
         }
@@ -276,6 +284,7 @@ struct FusedParams {
   int PA, LO;             // points per axis, outer points per axis
   long long T_pad;
   long long a_lo_row, b_lo_row;
+  int P, vblk;
   float* Mp;
 };
 
@@ -333,9 +342,16 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
             const uint32_t fb = smem_u32(&full[st]);
             mbar_expect_tx(fb, stage);
             const uint32_t dst = base + (uint32_t)st * stage;
-            const long long row = (long long)xi * p.T_pad + (long long)mb * kBM;
+            long long row, lrow;
+            if (p.vblk) {
+              row = ((long long)mb * p.P + xi) * (2 * kBM);
+              lrow = row + kBM;
+            } else {
+              row = (long long)xi * p.T_pad + (long long)mb * kBM;
+              lrow = p.a_lo_row + row;
+            }
             tma_load_2d(dst, &mapV, fb, kb * kBK, (int)row);
-            if (p.lo) tma_load_2d(dst + a_plane, &mapV, fb, kb * kBK, (int)(p.a_lo_row + row));
+            if (p.lo) tma_load_2d(dst + a_plane, &mapV, fb, kb * kBK, (int)lrow);
             tma_load_2d(dst + a_bytes, &mapU, fb, kb * kBK, xi * p.N);
             if (p.lo) tma_load_2d(dst + a_bytes + b_plane, &mapU, fb, kb * kBK, (int)(p.b_lo_row + (long long)xi * p.N));
             if (++st == p.nst) { st = 0; ph ^= 1; }
@@ -459,6 +475,7 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   prm.T_pad = g.T_pad;
   prm.a_lo_row = (long long)g.P * g.T_pad;
   prm.b_lo_row = (long long)g.P * g.cout_pad;
+  prm.vblk = (g.vblk && prm.lo) ? 1 : 0;
   prm.M = M;
   const uint32_t a_stage = tc::kBM * tc::kBK * 2 * (prm.lo ? 2 : 1);
   const uint32_t b_stage = (uint32_t)prm.N * tc::kBK * 2 * (prm.lo ? 2 : 1);
@@ -523,6 +540,8 @@ nw_status_t launch_gemm_tc_fused(const nw_plan_st* p, const Geometry& g, const v
   prm.T_pad = g.T_pad;
   prm.a_lo_row = (long long)g.P * g.T_pad;
   prm.b_lo_row = (long long)g.P * g.cout_pad;
+  prm.P = g.P;
+  prm.vblk = (g.vblk && prm.lo) ? 1 : 0;
   prm.Mp = Mp;
   const uint32_t stage = (tc::kBM * tc::kBK * 2 + (uint32_t)prm.N * tc::kBK * 2) * (prm.lo ? 2 : 1);
   prm.nst = (int)((200u * 1024u) / stage);
