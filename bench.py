@@ -149,7 +149,7 @@ def kernel_work(layer, info, math):
     x_b = layer.N * layer.Cin * layer.H * layer.W * es
     y_b = layer.N * layer.Cout * layer.Ho * layer.Wo * es
     v_b = P * T * cin_e * 4          # fp32 or bf16 hi+lo
-    m_b = P * T * cout_e * 4
+    m_b = info["m_rows"] * T * cout_e * 4   # M, or M' (inner output level fused into the contraction)
     u_b = P * cout_e * cin_e * 4
     passes = {"bf16x3": 3, "bf16": 1, "fp32": 1}[math]
     flops = 2 * P * T * cin_e * cout_e

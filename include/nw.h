@@ -103,6 +103,8 @@ typedef struct {
   int cin_pad, cout_pad; /* cin_e / cout_e rounded up to the tensor-core granule (16) */
   int math, dtype;
   size_t filter_bytes; /* bytes of U for nw_transform_filter */
+  int m_rows;          /* transform-domain rows per slice the contraction writes: points, or
+                          P_a * l_o * m_i when the inner output level is fused into its epilogue */
 } nw_plan_info_t;
 
 /* Create a plan for a K x K convolution with the given stride (1 or 2) using

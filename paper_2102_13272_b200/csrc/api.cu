@@ -152,9 +152,11 @@ extern "C" {
 // `stream` waits for the last device -> host copy before anything enqueued
 // after this call.
 static int host_chunk(int N) {
-  int nc = (N + 7) / 8;         // <= 8 chunks
-  if (nc < 2) nc = N < 2 ? N : 2;
-  return nc;
+  // images per full chunk: ~NW_HOST_CHUNKS chunks (default 8); the schedule ramps up and
+  // down around it so the pipeline fill (first H2D) and drain (last D2H) stay short
+  const int k = env_int("NW_HOST_CHUNKS", 8);
+  int nc = (N + (k > 0 ? k : 1) - 1) / (k > 0 ? k : 1);
+  return nc < 1 ? 1 : nc;
 }
 
 static void host_layout(const nw_plan_st *p, int N, int H, int W, size_t *fw, size_t *xb, size_t *yb, int *nc) {
@@ -208,7 +210,23 @@ nw_status_t nw_conv_forward_host(nw_plan_t p, const void *x_host, const void *U,
     if (!p->s_h2d && cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking) != cudaSuccess) return NW_ERR_CUDA;
     if (!p->s_d2h && cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking) != cudaSuccess) return NW_ERR_CUDA;
   }
-  const int nchunks = (N + nc - 1) / nc;
+  // chunk schedule: ramp 1, 2, 4 .. up to nc images, nc-image chunks, ramp back down, so the
+  // unoverlapped first copy in and last copy out are one image each
+  std::vector<int> sizes;
+  {
+    std::vector<int> head;
+    int hs = 0;
+    for (int c = 1; c < nc; c *= 2) { head.push_back(c); hs += c; }
+    if (2 * hs >= N) {
+      sizes.assign(N, 1);
+    } else {
+      sizes = head;
+      int mid = N - 2 * hs;
+      while (mid > 0) { const int c = mid < nc ? mid : nc; sizes.push_back(c); mid -= c; }
+      sizes.insert(sizes.end(), head.rbegin(), head.rend());
+    }
+  }
+  const int nchunks = (int)sizes.size();
   // events: [0] start, per chunk: in (x landed), comp (forward done), out (y copied)
   std::vector<cudaEvent_t> ev(1 + 3 * (size_t)nchunks, nullptr);
   for (auto &e : ev)
@@ -218,8 +236,9 @@ nw_status_t nw_conv_forward_host(nw_plan_t p, const void *x_host, const void *U,
   auto E_out = [&](int k) { return ev[3 + 3 * k]; };
   bool ok = cudaEventRecord(ev[0], s) == cudaSuccess && cudaStreamWaitEvent(p->s_h2d, ev[0], 0) == cudaSuccess &&
             cudaStreamWaitEvent(p->s_d2h, ev[0], 0) == cudaSuccess;
-  for (int k = 0; ok && k < nchunks; ++k) {
-    const int n0 = k * nc, nk = (N - n0) < nc ? (N - n0) : nc, b = k & 1;
+  int n0 = 0;
+  for (int k = 0; ok && k < nchunks; n0 += sizes[k], ++k) {
+    const int nk = sizes[k], b = k & 1;
     if (k >= 2) ok = ok && cudaStreamWaitEvent(p->s_h2d, E_comp(k - 2), 0) == cudaSuccess;  // x buffer free
     ok = ok && cudaMemcpyAsync(xd[b], static_cast<const char *>(x_host) + (size_t)n0 * ximg, (size_t)nk * ximg,
                                cudaMemcpyHostToDevice, p->s_h2d) == cudaSuccess;

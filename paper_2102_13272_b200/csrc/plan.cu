@@ -277,6 +277,10 @@ nw_status_t nw_plan_info(nw_plan_t p, nw_plan_info_t *info) {
   info->cin_pad = p->cin_pad; info->cout_pad = p->cout_pad;
   info->math = p->math; info->dtype = p->dtype;
   info->filter_bytes = filter_bytes(p);
+  {
+    Geometry g = make_geometry(p, 1, 3 * p->K + 16, 3 * p->K + 16);
+    info->m_rows = gemm_fused_eligible(p, g) ? p->ax.Pa * p->ax.l_o * p->m_i : info->points;
+  }
   return NW_OK;
 }
 
