@@ -33,9 +33,10 @@ struct InCfg {
   static constexpr int ROWS = SR * (X::SHMAX + X::L);           // raw window rows
   static constexpr int CSTR = WSC | 1;                          // odd channel stride in Hs
   static constexpr int NPAIR = CC * SR * SR / 2;                // ce pairs per block
-  static constexpr int HS = X::NPH * SR * X::PA * CC * CSTR;    // floats
+  static constexpr int PROWS = X::SHMAX + X::L;                 // window rows of one stride phase
+  static constexpr int HS = X::NPH * X::PA * CC * CSTR;         // floats (one row phase at a time)
   static constexpr size_t SMEM = (size_t)HS * sizeof(float);
-  static constexpr int THREADS = (CC * SR >= 64) ? 512 : (CC * SR >= 32) ? 256 : 128;
+  static constexpr int THREADS = (CC >= 64) ? 512 : (CC >= 32 || SR == 2) ? 256 : 128;
   static constexpr int MINB = 512 / THREADS;                    // resident CTAs per SM (registers <= 128)
 };
 
@@ -123,6 +124,13 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
   const int row0 = SR * (ah * X::ADV) + g.off[0];
   const int col0 = SR * (aw0 * X::ADV) + g.off[0];
 
+  const long long pstride = (long long)g.T_pad * g.cin_pad;  // elements between consecutive points
+  const long long plane = (long long)g.P * pstride;          // hi -> lo plane (bf16 elements)
+  // stride 2: the two row phases p of the polyphase split (Eq. 2.7) run one after the
+  // other through the same shared buffer (half the footprint, twice the resident CTAs)
+#pragma unroll 1
+  for (int p = 0; p < SR; ++p) {
+  if (p) __syncthreads();  // pass 2 of the previous phase is done with Hs
   // ---------------- pass 1: columns along h (straight from x) ----------------
 #pragma unroll 1
   for (int task = tid; task < CC * C::WSC; task += C::THREADS) {
@@ -130,48 +138,42 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
     const int ci = cin0 + c, gc = col0 + col;
     const bool cok = ci < g.Cin && gc >= 0 && gc < g.W;
     const XT* src = x + (((long long)n * g.Cin + (cok ? ci : 0)) * g.H) * g.W + (cok ? gc : 0);
-    float xr[C::ROWS];
-    const XT* rp = src + (long long)row0 * g.W;
+    float xr[C::PROWS];
+    const XT* rp = src + (long long)(row0 + p) * g.W;
 #pragma unroll
-    for (int r = 0; r < C::ROWS; ++r) {
-      const int gr = row0 + r;
+    for (int r = 0; r < C::PROWS; ++r) {
+      const int gr = row0 + p + SR * r;
       xr[r] = (cok && gr >= 0 && gr < g.H) ? to_f(*rp) : 0.f;
-      long long w = g.W;
+      long long w = (long long)SR * g.W;
       asm volatile("" : "+l"(w));
       rp += w;
     }
 #pragma unroll
     for (int ph = 0; ph < NPH; ++ph) {
       const int sh = ph == 0 ? 0 : SH1;
+      float xin[L], hv[PA];
 #pragma unroll
-      for (int p = 0; p < SR; ++p) {
-        float xin[L], hv[PA];
+      for (int r = 0; r < L; ++r) xin[r] = xr[sh + r];
+      in_axis<MO, RO, MI>(xin, hv);
+      float* dst = Hs + (ph * PA * CC + c) * C::CSTR + col;
 #pragma unroll
-        for (int r = 0; r < L; ++r) xin[r] = xr[SR * (sh + r) + p];
-        in_axis<MO, RO, MI>(xin, hv);
-        float* dst = Hs + ((ph * SR + p) * PA * CC + c) * C::CSTR + col;
-#pragma unroll
-        for (int q = 0; q < PA; ++q) dst[q * CC * C::CSTR] = hv[q];
-      }
+      for (int q = 0; q < PA; ++q) dst[q * CC * C::CSTR] = hv[q];
     }
   }
   __syncthreads();
 
   // ---------------- pass 2: rows along w, split, store V ----------------
-  const long long pstride = (long long)g.T_pad * g.cin_pad;  // elements between consecutive points
-  const long long plane = (long long)g.P * pstride;          // hi -> lo plane (bf16 elements)
-  constexpr int NTASK = NPH * NPH * SR * PA * C::TW * (CC * SR / 2);
+  constexpr int NPR = (SR == 1) ? CC / 2 : CC;  // channel pairs (stride 1) / channels with both column phases
+  constexpr int NTASK = NPH * NPH * PA * C::TW * NPR;
 #pragma unroll 1
   for (int task = tid; task < NTASK; task += C::THREADS) {
     int r = task;
-    const int pr = r % (CC * SR / 2);  // pair within (row phase p): stride 1 channel pair, stride 2 channel
-    r /= (CC * SR / 2);
+    const int pr = r % NPR;
+    r /= NPR;
     const int tile = r % C::TW;
     r /= C::TW;
     const int p_h = r % PA;
     r /= PA;
-    const int p = r % SR;
-    r /= SR;
     const int pw = r % NPH;
     const int phh = r / NPH;
     const int aw = aw0 + tile;
@@ -183,8 +185,8 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
       c0 = c1 = pr; q0 = 0; q1 = 1;
       ce = (cin0 + pr) * 4 + p * 2;
     }
-    const float* h0 = Hs + (((phh * SR + p) * PA + p_h) * CC + c0) * C::CSTR;
-    const float* h1 = Hs + (((phh * SR + p) * PA + p_h) * CC + c1) * C::CSTR;
+    const float* h0 = Hs + ((phh * PA + p_h) * CC + c0) * C::CSTR;
+    const float* h1 = Hs + ((phh * PA + p_h) * CC + c1) * C::CSTR;
     const int cb = tile * X::ADV + (pw == 0 ? 0 : SH1);
     if (aw >= g.tiles_w || ce >= g.cin_pad) continue;
     float za[X::LO][X::LI], zb[X::LO][X::LI];
@@ -215,6 +217,7 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
       store_row<MO, RO, MI, BF>(za, zb, hp, hp + plane * ES, pstride * ES);
     }
   }
+  }  // row phase p
 }
 
 template <int MO, int RO, int MI, int SR, int CC, typename XT, bool BF, int CINP>
@@ -255,7 +258,10 @@ static nw_status_t input_pick(const Geometry& g, const void* x, void* V, cudaStr
     const char* v = getenv("NW_IN_CC");
     return v ? atoi(v) : 32;
   }();
-  if (SR == 2) return input_launch<MO, RO, MI, SR, 8, XT, BF>(g, x, V, s);
+  if (SR == 2) {  // 4 contraction channels per source channel; narrow layers (C4a: 3) take 8-channel CTAs
+    if (g.cin_pad / 4 <= 8) return input_launch<MO, RO, MI, SR, 8, XT, BF>(g, x, V, s);
+    return input_launch<MO, RO, MI, SR, 16, XT, BF>(g, x, V, s);
+  }
   if (Ax<MO, RO, MI>::NPH == 1) {
     if (cc >= 64 && g.cin_pad >= 64 && InCfg<MO, RO, MI, SR, 64>::SMEM <= 227 * 1024)
       return input_launch<MO, RO, MI, SR, 64, XT, BF>(g, x, V, s);

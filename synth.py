@@ -64,23 +64,23 @@ CONFIGS: Dict[str, Layer] = {
     # configs[0]: parity config, F(2,3)(x)F(2,3) with coverage phases
     "c1": Layer("c1", 1, 16, 16, 32, 32, 5, 1, 2, m_o=2, m_i=2, xdist="unif11", wdist="unif11", seed=1),
     # configs[1]: filter-size sweep (the bench workload)
-    # (nesting F(4,3) (x) F(3,3): 12x12-output slices; the fastest outer kernel that meets the
-    #  5e-3 gate with margin -- DESIGN.md#R20)
+    # (nesting F(4,3) (x) F(3,3) for configs[1..4]: 12x12-output slices; the fastest outer
+    #  kernel that meets the 5e-3 gate with margin -- DESIGN.md#R20)
     "c2k5": Layer("c2k5", 32, 64, 64, 128, 128, 5, 1, 2, m_o=4, seed=21),
     "c2k7": Layer("c2k7", 32, 64, 64, 128, 128, 7, 1, 3, m_o=4, seed=22),
     "c2k9": Layer("c2k9", 32, 64, 64, 128, 128, 9, 1, 4, m_o=4, seed=23),
     # configs[2]: large-filter bf16 layer
     "c3": Layer("c3", 64, 256, 256, 64, 64, 9, 1, 4, m_o=4, dtype="bf16", xdist="relu_normal", seed=3),
     # configs[3]: strided large filters (stride-Winograd phases)
-    "c4a": Layer("c4a", 256, 3, 64, 224, 224, 7, 2, 3, xdist="unif01", seed=41),
-    "c4b": Layer("c4b", 256, 64, 64, 112, 112, 9, 2, 4, xdist="unif01", seed=42),
+    "c4a": Layer("c4a", 256, 3, 64, 224, 224, 7, 2, 3, m_o=4, xdist="unif01", seed=41),
+    "c4b": Layer("c4b", 256, 64, 64, 112, 112, 9, 2, 4, m_o=4, xdist="unif01", seed=42),
     # configs[4]: FSRCNN-s shaped network, nested layers first and last
-    "c5_conv1": Layer("c5_conv1", 16, 1, 32, 540, 960, 5, 1, 2, xdist="unif01", seed=5, prelu=True),
+    "c5_conv1": Layer("c5_conv1", 16, 1, 32, 540, 960, 5, 1, 2, m_o=4, xdist="unif01", seed=5, prelu=True),
     "c5_conv2": Layer("c5_conv2", 16, 32, 5, 540, 960, 1, 1, 0, seed=51, prelu=True),
     "c5_conv3": Layer("c5_conv3", 16, 5, 5, 540, 960, 3, 1, 1, seed=52, prelu=True),
     "c5_conv4": Layer("c5_conv4", 16, 5, 32, 540, 960, 1, 1, 0, seed=53, prelu=True),
     "c5_deconv": Layer("c5_deconv", 16, 32, 1, 540, 960, 9, 2, 4, transposed=True, output_padding=1,
-                       seed=54),
+                       m_o=4, seed=54),
 }
 
 C2_SWEEP = ["c2k5", "c2k7", "c2k9"]
