@@ -132,32 +132,74 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
   for (int p = 0; p < SR; ++p) {
   if (p) __syncthreads();  // pass 2 of the previous phase is done with Hs
   // ---------------- pass 1: columns along h (straight from x) ----------------
-#pragma unroll 1
-  for (int task = tid; task < CC * C::WSC; task += C::THREADS) {
+  // fp32 x: every load of the thread's NT1 columns is issued before the first transform,
+  // so a CTA waits for one global round trip per row phase instead of one per column
+  // (measured faster for C2; bf16 x (C3) keeps the column-at-a-time loop, which measured faster)
+  if constexpr (sizeof(XT) == 4) {
+  constexpr int NT1 = (CC * C::WSC + C::THREADS - 1) / C::THREADS;
+  float xr[NT1][C::PROWS];
+#pragma unroll
+  for (int i = 0; i < NT1; ++i) {
+    const int task = tid + i * C::THREADS;
     const int col = task % C::WSC, c = task / C::WSC;
     const int ci = cin0 + c, gc = col0 + col;
-    const bool cok = ci < g.Cin && gc >= 0 && gc < g.W;
-    const XT* src = x + (((long long)n * g.Cin + (cok ? ci : 0)) * g.H) * g.W + (cok ? gc : 0);
-    float xr[C::PROWS];
-    const XT* rp = src + (long long)(row0 + p) * g.W;
+    const bool cok = task < CC * C::WSC && ci < g.Cin && gc >= 0 && gc < g.W;
+    const XT* rp = x + (((long long)n * g.Cin + (cok ? ci : 0)) * g.H) * g.W + (cok ? gc : 0) +
+                   (long long)(row0 + p) * g.W;
 #pragma unroll
     for (int r = 0; r < C::PROWS; ++r) {
       const int gr = row0 + p + SR * r;
-      xr[r] = (cok && gr >= 0 && gr < g.H) ? to_f(*rp) : 0.f;
+      xr[i][r] = (cok && gr >= 0 && gr < g.H) ? to_f(*rp) : 0.f;
       long long w = (long long)SR * g.W;
       asm volatile("" : "+l"(w));
       rp += w;
     }
+  }
+#pragma unroll
+  for (int i = 0; i < NT1; ++i) {
+    const int task = tid + i * C::THREADS;
+    if (task >= CC * C::WSC) break;
+    const int col = task % C::WSC, c = task / C::WSC;
 #pragma unroll
     for (int ph = 0; ph < NPH; ++ph) {
       const int sh = ph == 0 ? 0 : SH1;
       float xin[L], hv[PA];
 #pragma unroll
-      for (int r = 0; r < L; ++r) xin[r] = xr[sh + r];
+      for (int r = 0; r < L; ++r) xin[r] = xr[i][sh + r];
       in_axis<MO, RO, MI>(xin, hv);
       float* dst = Hs + (ph * PA * CC + c) * C::CSTR + col;
 #pragma unroll
       for (int q = 0; q < PA; ++q) dst[q * CC * C::CSTR] = hv[q];
+    }
+  }
+  } else {
+#pragma unroll 1
+    for (int task = tid; task < CC * C::WSC; task += C::THREADS) {
+      const int col = task % C::WSC, c = task / C::WSC;
+      const int ci = cin0 + c, gc = col0 + col;
+      const bool cok = ci < g.Cin && gc >= 0 && gc < g.W;
+      const XT* rp = x + (((long long)n * g.Cin + (cok ? ci : 0)) * g.H) * g.W + (cok ? gc : 0) +
+                     (long long)(row0 + p) * g.W;
+      float xc[C::PROWS];
+#pragma unroll
+      for (int r = 0; r < C::PROWS; ++r) {
+        const int gr = row0 + p + SR * r;
+        xc[r] = (cok && gr >= 0 && gr < g.H) ? to_f(*rp) : 0.f;
+        long long w = (long long)SR * g.W;
+        asm volatile("" : "+l"(w));
+        rp += w;
+      }
+#pragma unroll
+      for (int ph = 0; ph < NPH; ++ph) {
+        const int sh = ph == 0 ? 0 : SH1;
+        float xin[L], hv[PA];
+#pragma unroll
+        for (int r = 0; r < L; ++r) xin[r] = xc[sh + r];
+        in_axis<MO, RO, MI>(xin, hv);
+        float* dst = Hs + (ph * PA * CC + c) * C::CSTR + col;
+#pragma unroll
+        for (int q = 0; q < PA; ++q) dst[q * CC * C::CSTR] = hv[q];
+      }
     }
   }
   __syncthreads();
