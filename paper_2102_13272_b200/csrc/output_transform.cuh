@@ -88,76 +88,25 @@ __device__ __forceinline__ float csel(const float (&v)[kMaxL], int i) {
   return r;
 }
 
-template <int MO, int RO, int MI, typename YT, bool PRE>
-__global__ void __launch_bounds__(OutCfg<MO, RO, MI, PRE>::THREADS, 1)
-    output_transform_kernel(const __grid_constant__ CUtensorMap mapM, YT* __restrict__ y, Geometry g,
-                            const float* __restrict__ slopes, int nunits, int ngroups) {
+template <int MO, int RO, int MI, typename YT, bool PRE, int PART>
+__device__ __forceinline__ void out_consume(const float* ring, uint64_t* full, uint64_t* empty, float* ystage,
+                                            long long* sinfo, YT* __restrict__ y, const Geometry& g,
+                                            const float* __restrict__ slopes, int nunits, int ngroups) {
   using X = Ax<MO, RO, MI>;
   using C = OutCfg<MO, RO, MI, PRE>;
-  constexpr int RL = C::RL;
   constexpr AxisF F = axis_f(MO, RO, MI);
   constexpr OutTables<MO, RO, MI> OT = make_out_tables<MO, RO, MI>();
-  constexpr int MA = X::MA, PA = X::PA, LO = X::LO, LI = X::LI, NPH = X::NPH;
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  // 128-byte aligned base derived from the shared array itself (keeps loads in the shared window: LDS, not LD)
-  uint8_t* base = smem_raw + ((128u - (ptx::smem_u32(smem_raw) & 127u)) & 127u);
-  float* ring = reinterpret_cast<float*>(base);
-  float* ystage = reinterpret_cast<float*>(base + C::RING_BYTES);
-  long long* sinfo = reinterpret_cast<long long*>(base + C::RING_BYTES + C::YST_BYTES);  // [CO][TS][2]
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + C::RING_BYTES + C::YST_BYTES + C::INFO_BYTES);
-  uint64_t* empty = full + C::NST;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < C::NST; ++i) {
-      ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&empty[i]), C::WARPS);
-    }
-    ptx::mbar_init_fence();
-  }
-  __syncthreads();
-
-  if (warp == C::WARPS) {
-    // ------------------------------ TMA producer ------------------------------
-    if (lane == 0) {
-      ptx::tma_prefetch(&mapM);
-      int st = 0;
-      uint32_t ph = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const int t0 = (u / ngroups) * C::TS, co0 = (u % ngroups) * C::CO;
-        for (int r = 0; r < PA; ++r) {
-          ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
-          const uint32_t fb = ptx::smem_u32(&full[st]);
-          ptx::mbar_expect_tx(fb, C::STAGE * 4);
-          ptx::tma_load_3d(ptx::smem_u32(ring + st * C::STAGE), &mapM, fb, t0, co0, r * RL);
-          if (++st == C::NST) { st = 0; ph ^= 1; }
-        }
-      }
-    }
-    return;
-  }
-
-  // -------------------------------- consumers ---------------------------------
+  constexpr int MA = X::MA, LO = X::LO, LI = X::LI, NPH = X::NPH;
+  constexpr int RL = C::RL;
   constexpr int QW = C::QW;
-  const int cw_ = warp / C::SPL, part = warp - cw_ * C::SPL;   // channel within unit, column part
-  const int T0 = part * C::TH;                                  // first outer output of this part
+  constexpr int T0 = PART * C::TH;                              // first outer output of this part
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cw_ = warp / C::SPL;                                // channel within unit
   float* yst = ystage + warp * C::YST;
   long long* info = sinfo + warp * (C::TS * 2);
   const long long HoWo = (long long)g.Ho * g.Wo;
   const int rowstride = (g.mode == 2) ? 2 * g.Wo : g.Wo;
   const int colstride = (g.mode == 2) ? 2 : 1;
-  // split parts: this part's rows of A_o^T (runtime-selected once)
-  float cwo[C::TH][LO];
-#pragma unroll
-  for (int k = 0; k < C::TH; ++k)
-#pragma unroll
-    for (int po = 0; po < LO; ++po) {
-      float c = 0.f;
-#pragma unroll
-      for (int t = 0; t < MO; ++t)
-        if (F.AoT[t][po] != 0.f) c = fmaf((T0 + k == t) ? 1.f : 0.f, F.AoT[t][po], c);
-      cwo[k][po] = c;
-    }
   int st = 0;
   uint32_t ph = 0;
   for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -215,16 +164,16 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI, PRE>::THREADS, 1)
             for (int t = 0; t < MO; ++t) qv[t * MI + s2] = o[t];
           }
         } else {
-          // this part's outer rows
+          // this part's outer rows (compile-time selection of the F(m_o, r_o) outputs)
 #pragma unroll
-          for (int k = 0; k < C::TH; ++k)
+          for (int s2 = 0; s2 < MI; ++s2) {
+            float col[LO], o[MO];
 #pragma unroll
-            for (int s2 = 0; s2 < MI; ++s2) {
-              float acc = 0.f;
+            for (int po = 0; po < LO; ++po) col[po] = uw[po][s2];
+            K1<MO, RO>::at(col, o);
 #pragma unroll
-              for (int po = 0; po < LO; ++po) acc = fmaf(cwo[k][po], uw[po][s2], acc);
-              qv[k * MI + s2] = acc;
-            }
+            for (int k = 0; k < C::TH; ++k) qv[k * MI + s2] = (T0 + k < MO) ? o[(T0 + k < MO) ? T0 + k : 0] : 0.f;
+          }
         }
 #pragma unroll
         for (int s = 0; s < MI; ++s) {
@@ -327,6 +276,71 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI, PRE>::THREADS, 1)
       }
     }
     __syncwarp();
+  }
+}
+
+template <int MO, int RO, int MI, typename YT, bool PRE>
+__global__ void __launch_bounds__(OutCfg<MO, RO, MI, PRE>::THREADS, 1)
+    output_transform_kernel(const __grid_constant__ CUtensorMap mapM, YT* __restrict__ y, Geometry g,
+                            const float* __restrict__ slopes, int nunits, int ngroups) {
+  using X = Ax<MO, RO, MI>;
+  using C = OutCfg<MO, RO, MI, PRE>;
+  constexpr int RL = C::RL;
+  constexpr AxisF F = axis_f(MO, RO, MI);
+  constexpr OutTables<MO, RO, MI> OT = make_out_tables<MO, RO, MI>();
+  constexpr int MA = X::MA, PA = X::PA, LO = X::LO, LI = X::LI, NPH = X::NPH;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  // 128-byte aligned base derived from the shared array itself (keeps loads in the shared window: LDS, not LD)
+  uint8_t* base = smem_raw + ((128u - (ptx::smem_u32(smem_raw) & 127u)) & 127u);
+  float* ring = reinterpret_cast<float*>(base);
+  float* ystage = reinterpret_cast<float*>(base + C::RING_BYTES);
+  long long* sinfo = reinterpret_cast<long long*>(base + C::RING_BYTES + C::YST_BYTES);  // [CO][TS][2]
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + C::RING_BYTES + C::YST_BYTES + C::INFO_BYTES);
+  uint64_t* empty = full + C::NST;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NST; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&empty[i]), C::WARPS);
+    }
+    ptx::mbar_init_fence();
+  }
+  __syncthreads();
+
+  if (warp == C::WARPS) {
+    // ------------------------------ TMA producer ------------------------------
+    if (lane == 0) {
+      ptx::tma_prefetch(&mapM);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int t0 = (u / ngroups) * C::TS, co0 = (u % ngroups) * C::CO;
+        for (int r = 0; r < PA; ++r) {
+          ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
+          const uint32_t fb = ptx::smem_u32(&full[st]);
+          ptx::mbar_expect_tx(fb, C::STAGE * 4);
+          ptx::tma_load_3d(ptx::smem_u32(ring + st * C::STAGE), &mapM, fb, t0, co0, r * RL);
+          if (++st == C::NST) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------- consumers ---------------------------------
+  // the column part is a template parameter, so each part's rows of A_o^T are compile-time
+  // constants (zero coefficients and unused outputs vanish from the instruction stream)
+  const int part = warp % C::SPL;
+  if constexpr (C::SPL == 1) {
+    out_consume<MO, RO, MI, YT, PRE, 0>(ring, full, empty, ystage, sinfo, y, g, slopes, nunits, ngroups);
+  } else if constexpr (C::SPL == 2) {
+    if (part == 0) out_consume<MO, RO, MI, YT, PRE, 0>(ring, full, empty, ystage, sinfo, y, g, slopes, nunits, ngroups);
+    else out_consume<MO, RO, MI, YT, PRE, 1>(ring, full, empty, ystage, sinfo, y, g, slopes, nunits, ngroups);
+  } else {
+    if (part == 0) out_consume<MO, RO, MI, YT, PRE, 0>(ring, full, empty, ystage, sinfo, y, g, slopes, nunits, ngroups);
+    else if (part == 1) out_consume<MO, RO, MI, YT, PRE, 1>(ring, full, empty, ystage, sinfo, y, g, slopes, nunits, ngroups);
+    else out_consume<MO, RO, MI, YT, PRE, 2>(ring, full, empty, ystage, sinfo, y, g, slopes, nunits, ngroups);
   }
 }
 
