@@ -39,7 +39,7 @@ struct OutCfg {
   // dealt round-robin): 9 warps allow 168 registers per thread, 13 allow 128.  The
   // kernel is latency-bound, so pre-reduced rows (18 instead of 30 values) buy 12
   // consumer warps for the split 12 x 12 tile.
-  static constexpr int CO = (SPL == 1) ? 8 : (SPL == 2 ? (PRE ? 6 : 4) : 3);
+  static constexpr int CO = (SPL == 1) ? 8 : (SPL == 2 ? 6 : 3);
   static constexpr int WARPS = CO * SPL;          // consumer warps
   static constexpr int TS = 32;  // slices per unit (lanes)
   static constexpr int NST = 4;  // ring depth (point rows)
