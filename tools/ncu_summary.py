@@ -107,6 +107,8 @@ def main():
     ap.add_argument("--math", default="bf16x3")
     ap.add_argument("--m-outer", type=int, default=4, help="outer kernel of the profiled plan")
     ap.add_argument("--note", default="")
+    ap.add_argument("--dram", nargs="*", default=[],
+                    help="lightweight ncu CSVs dram_<tag>_<layer>.csv (gpu__time_duration, dram bytes)")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     md = [f"# ncu summary {a.tag}", ""]
@@ -134,6 +136,31 @@ def main():
                 for key, kind in KIND.items():
                     if key in d["kernel"]:
                         traffic[f"{kind}:{a.math}:{layer}:m{a.m_outer}"] = int(b)
+    for path in a.dram:
+        layer = os.path.basename(path)[:-4].split("_")[-1]
+        rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+        h = rows[0]
+        ki, mi, vi, ui = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
+        ids = h.index("ID")
+        per = collections.defaultdict(lambda: collections.defaultdict(float))
+        for r in rows[1:]:
+            if r[mi].startswith("dram__bytes"):
+                per[(short(r[ki]), r[ids])]["bytes"] += to_bytes(r[vi], r[ui] or "byte")
+            elif r[mi] == "gpu__time_duration.sum":
+                per[(short(r[ki]), r[ids])]["ns"] += float(r[vi].replace(",", ""))
+        agg = collections.defaultdict(list)
+        for (kname, _), d in per.items():
+            agg[kname].append(d)
+        md += [f"## dram bytes per launch, {layer} (`{os.path.basename(path)}`)", "",
+               "| kernel | launches | dram read+write per launch | time per launch |", "|---|---|---|---|"]
+        for kname, lst in agg.items():
+            b = sum(d["bytes"] for d in lst) / len(lst)
+            t = sum(d["ns"] for d in lst) / len(lst)
+            md.append(f"| {kname} | {len(lst)} | {b / 1e6:.1f} MB | {t / 1e3:.1f} us |")
+            for key, kind in KIND.items():
+                if key in kname:
+                    traffic[f"{kind}:{a.math}:{layer}:m{a.m_outer}"] = int(b)
+        md.append("")
     json.dump(traffic, open(tfile, "w"), indent=1, sort_keys=True)
     if a.bench:
         line = [l for l in open(a.bench).read().splitlines() if l.startswith("{")][-1]
