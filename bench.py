@@ -38,8 +38,10 @@ WORKLOADS = {
     "c3": ["c3"],
     "c4": ["c4a", "c4b"],
     "c5": ["c5_conv1", "c5_deconv"],
+    "table1": synth.TABLE1,
 }
 WORKLOAD_DESC = {
+    "table1": "paper Table I conv2d shapes (P:154-160): SRCNN 9x9 64<-1, 5x5 32<-64, 5x5 1<-32, 256x256, N=8, fp32",
     "c1": "configs[0]: 5x5 s1 p2, N=1, Cin=Cout=16, 32x32, fp32, F(2,3)(x)F(2,3) + coverage phases",
     "c2": "configs[1]: filter-size sweep K in {5,7,9}, s1 same pad, N=32, Cin=Cout=64, 128x128, fp32",
     "c3": "configs[2]: 9x9 s1 p4, N=64, Cin=Cout=256, 64x64, bf16 storage, fp32 accumulate",
@@ -344,7 +346,8 @@ def main():
         for path in ("ola", "direct"):
             try:
                 tot = 0.0
-                for conv, x, y in zip(convs, xs, ys):
+                lay = []
+                for l, conv, x, y, pl in zip(layers_all, convs, xs, ys, per_layer):
                     conv.workspace(x.shape[0], x.shape[2], x.shape[3], path)
                     conv(x, y, path=path)
                     torch.cuda.synchronize()
@@ -354,9 +357,15 @@ def main():
                         conv(x, y, path=path)
                     e1.record()
                     torch.cuda.synchronize()
-                    tot += e0.elapsed_time(e1) / 3
+                    lm = e0.elapsed_time(e1) / 3
+                    tot += lm
+                    lay.append({"layer": l.name, "ms": round(lm, 4), "nested_speedup": round(lm / pl["ms"], 3)})
                 compare[path] = {"ms_per_step": round(tot, 4),
-                                 "tflops_direct_equiv": round(flops_rank / (tot / 1e3) / 1e12, 2)}
+                                 "tflops_direct_equiv": round(flops_rank / (tot / 1e3) / 1e12, 2),
+                                 "per_layer": lay}
+                if args.workload == "table1" and path == "ola":
+                    compare[path]["paper_nested_speedup_fpga"] = {
+                        n: synth.TABLE1_PAPER_SPEEDUP[n] for n in WORKLOADS["table1"]}
             except nw.NWError as e:
                 compare[path] = {"unavailable": str(e)}
             except RuntimeError as e:  # out of memory etc.

@@ -83,6 +83,18 @@ CONFIGS: Dict[str, Layer] = {
                        m_o=4, seed=54),
 }
 
+# Table I of the paper (ZCU102): the conv2d layer shapes (Cout, Cin, H, W), measured
+# there as nested vs OLA-Winograd GOPs.  Weights / images of SRCNN are not available: the
+# synthetic stand-ins use BASELINE configs[1]'s distributions; batch 8 (the paper runs one image).
+# The depthwise PNASNet 7x7 row needs a depthwise path, which is not built.
+CONFIGS.update({
+    "t1_srcnn9": Layer("t1_srcnn9", 8, 1, 64, 256, 256, 9, 1, 4, m_o=4, seed=61),
+    "t1_srcnn5a": Layer("t1_srcnn5a", 8, 64, 32, 256, 256, 5, 1, 2, m_o=4, seed=62),
+    "t1_srcnn5b": Layer("t1_srcnn5b", 8, 32, 1, 256, 256, 5, 1, 2, m_o=4, seed=63),
+})
+TABLE1 = ["t1_srcnn9", "t1_srcnn5a", "t1_srcnn5b"]
+TABLE1_PAPER_SPEEDUP = {"t1_srcnn9": 3.29, "t1_srcnn5a": 1.43, "t1_srcnn5b": 1.43}
+
 C2_SWEEP = ["c2k5", "c2k7", "c2k9"]
 C5_NET = ["c5_conv1", "c5_conv2", "c5_conv3", "c5_conv4", "c5_deconv"]
 PRELU_SLOPE = 0.25

@@ -139,3 +139,15 @@ def test_larger_outer_tile(m_o, name, math):
     ref = _ref(layer, t)
     tol = TOL[math] if layer.dtype == "f32" else max(TOL[math], 2.0 ** -8)
     assert rel_err(y, ref) <= tol
+
+
+@pytest.mark.parametrize("name", ["t1_srcnn9", "t1_srcnn5a", "t1_srcnn5b"])
+@pytest.mark.parametrize("path", ["nested", "ola"])
+def test_table1_shapes(name, path):
+    # Table I layer shapes at a reduced image size, bf16x3
+    from paper_2102_13272_b200 import NestedConv2d
+    layer = synth.small(synth.CONFIGS[name], N=2, H=37, W=30)
+    t = synth.make_inputs(layer)
+    conv = NestedConv2d(t["w"].cuda(), 1, layer.pad, layer.m_o, layer.m_i, _math("bf16x3"))
+    y = conv(t["x"].cuda(), path=path).cpu().numpy()
+    assert rel_err(y, _ref(layer, t)) <= TOL["bf16x3"]
