@@ -277,7 +277,7 @@ def main():
         t = synth.make_inputs(l.with_(seed=l.seed + 1000 * rank)) if rank else synth.make_inputs(l)
         w = synth.make_inputs(l, x=False)["w"].to(dev)     # same weights on every rank
         slopes = torch.full((l.Cout,), synth.PRELU_SLOPE, device=dev) if l.prelu else None
-        conv = nw.NestedConv2d(w, l.stride, l.pad, l.m_o, l.m_i, math, transposed=l.transposed,
+        conv = nw.NestedConv2d(w, l.stride, l.pad, l.m_o, l.m_i, math, transposed=l.transposed, outer_taps=l.r_o,
                                output_padding=l.output_padding, prelu_slopes=slopes)
         # filter transform once on rank 0 (timed separately), broadcast U over NCCL
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -422,7 +422,8 @@ def main():
             "dtype": {"bf16x3": "bf16x3", "fp32": "f32", "bf16": "bf16"}[args.math],
             "data": "synthetic (seeded; BASELINE distributions, DESIGN.md input recipe)",
             "config": {"workload": WORKLOAD_DESC[args.workload], "layers": [l.name for l in layers_all],
-                       "nesting": [f"F({l.m_o},3)(x)F({l.m_i},3)" for l in layers_all],
+                       "nesting": [f"F({c.info['m_outer']},{c.info['r_outer']})(x)F({c.info['m_inner']},3)"
+                                   for c in convs],
                        "path": args.path, "math": args.math, "images_per_rank": layers_all[0].N,
                        "l2": "no flush: x (>=134 MB) and V/M (>1 GB per layer) exceed the 126 MB L2",
                        "step": "input transform + contraction + output transform per layer (nw_conv_forward)"},

@@ -21,6 +21,8 @@ nw_status_t output_impl_pre(const nw_plan_st*, const Geometry&, const float*, vo
     if (mo_ == 1 && ro_ == 1 && mi_ == 3) return FN<1, 1, 3>(__VA_ARGS__); \
     if (mo_ == 4 && ro_ == 3 && mi_ == 3) return FN<4, 3, 3>(__VA_ARGS__); \
     if (mo_ == 5 && ro_ == 3 && mi_ == 3) return FN<5, 3, 3>(__VA_ARGS__); \
+    if (mo_ == 4 && ro_ == 2 && mi_ == 3) return FN<4, 2, 3>(__VA_ARGS__); \
+    if (mo_ == 5 && ro_ == 2 && mi_ == 3) return FN<5, 2, 3>(__VA_ARGS__); \
     return NW_ERR_UNSUPPORTED;                                             \
   } while (0)
 

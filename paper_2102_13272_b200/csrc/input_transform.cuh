@@ -317,7 +317,7 @@ static nw_status_t input_pick(const Geometry& g, const void* x, void* V, cudaStr
 template <int MO, int RO, int MI>
 nw_status_t input_impl(const nw_plan_st* p, const Geometry& g, const void* x, void* V, cudaStream_t s) {
   // stride 2 and bf16 storage are built for the F(m_o,3) (x) F(3,3) plans and the OLA kernel
-  constexpr bool kFull = (RO == 3 && MI == 3 && MO >= 3) || (MO == 1 && RO == 1 && MI == 3);
+  constexpr bool kFull = (RO >= 2 && MI == 3 && MO >= 3) || (MO == 1 && RO == 1 && MI == 3);
   constexpr bool kBf16In = kFull || (MO == 2 && RO == 3 && MI == 2);
   const bool bf = p->math != NW_MATH_FP32_SIMT;
   const bool xb = p->dtype == NW_DTYPE_BF16;

@@ -40,7 +40,7 @@ def test_writes_stay_in_bounds(name, kw, math, path):
     layer = synth.small(synth.CONFIGS[name], **kw) if kw else synth.CONFIGS[name]
     t = synth.make_inputs(layer)
     slopes = torch.full((layer.Cout,), synth.PRELU_SLOPE, device="cuda") if layer.prelu else None
-    conv = NestedConv2d(t["w"].cuda(), layer.stride, layer.pad, layer.m_o, layer.m_i, _math(math),
+    conv = NestedConv2d(t["w"].cuda(), layer.stride, layer.pad, layer.m_o, layer.m_i, _math(math), outer_taps=layer.r_o,
                         transposed=layer.transposed, output_padding=layer.output_padding, prelu_slopes=slopes)
     x = t["x"].cuda()
     N, _, H, W = x.shape

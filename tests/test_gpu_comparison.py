@@ -21,7 +21,7 @@ def _run(layer, math, path):
     t = synth.make_inputs(layer)
     x, w = t["x"].cuda(), t["w"].cuda()
     slopes = torch.full((layer.Cout,), synth.PRELU_SLOPE, device="cuda") if layer.prelu else None
-    conv = NestedConv2d(w, layer.stride, layer.pad, layer.m_o, layer.m_i, _math(math),
+    conv = NestedConv2d(w, layer.stride, layer.pad, layer.m_o, layer.m_i, _math(math), outer_taps=layer.r_o,
                         transposed=layer.transposed, output_padding=layer.output_padding,
                         prelu_slopes=slopes)
     y = conv(x, path=path)

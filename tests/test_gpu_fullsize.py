@@ -42,7 +42,7 @@ def test_full_size_sampled(name):
     layer = synth.CONFIGS[name]
     t = synth.make_inputs(layer)
     slopes = torch.full((layer.Cout,), synth.PRELU_SLOPE, device="cuda") if layer.prelu else None
-    conv = NestedConv2d(t["w"].cuda(), layer.stride, layer.pad, layer.m_o, layer.m_i, _math("bf16x3"),
+    conv = NestedConv2d(t["w"].cuda(), layer.stride, layer.pad, layer.m_o, layer.m_i, _math("bf16x3"), outer_taps=layer.r_o,
                         transposed=layer.transposed, output_padding=layer.output_padding, prelu_slopes=slopes)
     y = conv(t["x"].cuda())
     torch.cuda.synchronize()

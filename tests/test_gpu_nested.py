@@ -30,7 +30,7 @@ def _run(layer, math, prelu=False):
     slopes = None
     if layer.prelu or prelu:
         slopes = torch.full((layer.Cout,), synth.PRELU_SLOPE, device="cuda")
-    conv = NestedConv2d(w, layer.stride, layer.pad, layer.m_o, layer.m_i, _math(math),
+    conv = NestedConv2d(w, layer.stride, layer.pad, layer.m_o, layer.m_i, _math(math), outer_taps=layer.r_o,
                         transposed=layer.transposed, output_padding=layer.output_padding,
                         prelu_slopes=slopes)
     y = conv(x)
@@ -129,12 +129,13 @@ def test_edge_shapes_bf16x3(N, H, W):
     assert rel_err(y, _ref(layer, t)) <= TOL["bf16x3"]
 
 
-@pytest.mark.parametrize("m_o", [3, 4, 5])
-@pytest.mark.parametrize("name", ["c2k5", "c2k7", "c2k9", "c3", "c4b", "c5_deconv"])
+@pytest.mark.parametrize("m_o,r_o", [(3, 3), (4, 3), (5, 3), (4, 0), (5, 0)])
+@pytest.mark.parametrize("name", ["c2k5", "c2k7", "c2k9", "c3", "c4a", "c4b", "c5_conv1", "c5_deconv"])
 @pytest.mark.parametrize("math", ["fp32", "bf16x3"])
-def test_larger_outer_tile(m_o, name, math):
-    # F(m_o,3) (x) F(3,3): (3 m_o) x (3 m_o) outputs per slice; same gates
-    layer = SMALL[name].with_(m_o=m_o)
+def test_larger_outer_tile(m_o, r_o, name, math):
+    # F(m_o, r_o) (x) F(3,3): (3 m_o) x (3 m_o) outputs per slice; r_o = 0 picks ceil(K'/3) taps
+    # (F(m_o, 2) for filters of <= 6 taps per phase); same gates (R8, #R20)
+    layer = SMALL[name].with_(m_o=m_o, r_o=r_o)
     t, y = _run(layer, math)
     ref = _ref(layer, t)
     tol = TOL[math] if layer.dtype == "f32" else max(TOL[math], 2.0 ** -8)
@@ -148,6 +149,6 @@ def test_table1_shapes(name, path):
     from paper_2102_13272_b200 import NestedConv2d
     layer = synth.small(synth.CONFIGS[name], N=2, H=37, W=30)
     t = synth.make_inputs(layer)
-    conv = NestedConv2d(t["w"].cuda(), 1, layer.pad, layer.m_o, layer.m_i, _math("bf16x3"))
+    conv = NestedConv2d(t["w"].cuda(), 1, layer.pad, layer.m_o, layer.m_i, _math("bf16x3"), outer_taps=layer.r_o)
     y = conv(t["x"].cuda(), path=path).cpu().numpy()
     assert rel_err(y, _ref(layer, t)) <= TOL["bf16x3"]
