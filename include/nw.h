@@ -28,6 +28,13 @@
  *  - A plan is immutable after its first use (finalize) and may be shared by
  *    several threads and streams; each concurrent call brings its own
  *    workspace.
+ *  - Environment tunables (performance only; results are bit-identical or within
+ *    rounding order, never a different algorithm): NW_FUSE_AI=0 disables the
+ *    inner output level in the contraction epilogue; NW_IN_CC=16|32|64 source
+ *    channels per input-transform CTA (default 32); NW_PIPE_CHUNKS=k runs
+ *    nw_conv_forward as a k-chunk three-stream pipeline (default 1) and
+ *    NW_GEMM_CTAS caps its contraction grid; NW_HOST_CHUNKS=k sets the chunk
+ *    count of nw_conv_forward_host (default 8).
  */
 #ifndef NW_H_
 #define NW_H_

@@ -101,12 +101,14 @@ nw_status_t launch_pack_input(const nw_plan_st* p, const Geometry& g, const void
   LaunchScope scope_("pack_input", s);
   if (p->dtype == NW_DTYPE_BF16) {
     auto k = bf ? pack_input_kernel<__nv_bfloat16, true> : pack_input_kernel<__nv_bfloat16, false>;
-    if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if ((bf ? ensure_smem<pack_input_kernel<__nv_bfloat16, true>>(200 * 1024)
+            : ensure_smem<pack_input_kernel<__nv_bfloat16, false>>(200 * 1024)) != NW_OK)
       return NW_ERR_CUDA;
     k<<<(unsigned)nb, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), V, g, wchunks);
   } else {
     auto k = bf ? pack_input_kernel<float, true> : pack_input_kernel<float, false>;
-    if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if ((bf ? ensure_smem<pack_input_kernel<float, true>>(200 * 1024)
+            : ensure_smem<pack_input_kernel<float, false>>(200 * 1024)) != NW_OK)
       return NW_ERR_CUDA;
     k<<<(unsigned)nb, 256, smem, s>>>(static_cast<const float*>(x), V, g, wchunks);
   }

@@ -266,12 +266,7 @@ template <int MO, int RO, int MI, int SR, int CC, typename XT, bool BF, int CINP
 static nw_status_t input_launch_c(const Geometry& g, const void* x, void* V, cudaStream_t s) {
   using C = InCfg<MO, RO, MI, SR, CC>;
   auto kern = input_transform_kernel<MO, RO, MI, SR, CC, XT, BF, CINP>;
-  static bool attr_done = false;  // per instantiation
-  if (!attr_done) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
-      return NW_ERR_CUDA;
-    attr_done = true;
-  }
+  if (ensure_smem<input_transform_kernel<MO, RO, MI, SR, CC, XT, BF, CINP>>((int)C::SMEM) != NW_OK) return NW_ERR_CUDA;
   const int wgroups = (g.tiles_w + C::TW - 1) / C::TW;
   const int cin_src = (SR == 1) ? g.cin_pad : g.cin_pad / 4;
   const int cgroups = (cin_src + CC - 1) / CC;

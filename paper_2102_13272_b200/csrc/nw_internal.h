@@ -126,4 +126,19 @@ inline nw_status_t check_launch() {
 
 inline long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
 
+// Raise kernel KERN's dynamic shared-memory limit once per device (function attributes are
+// per device; one bit per device id, thread-safe).
+template <auto KERN>
+inline nw_status_t ensure_smem(int bytes) {
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return NW_ERR_CUDA;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return NW_OK;
+  if (cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return NW_ERR_CUDA;
+  done.fetch_or(bit, std::memory_order_release);
+  return NW_OK;
+}
+
 }  // namespace nw

@@ -349,12 +349,7 @@ static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const f
   using C = OutCfg<MO, RO, MI, PRE>;
   using X = Ax<MO, RO, MI>;
   auto kern = output_transform_kernel<MO, RO, MI, YT, PRE>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
-      return NW_ERR_CUDA;
-    attr_done = true;
-  }
+  if (ensure_smem<output_transform_kernel<MO, RO, MI, YT, PRE>>((int)C::SMEM) != NW_OK) return NW_ERR_CUDA;
   alignas(64) CUtensorMap map;
   const uint64_t rows = PRE ? (uint64_t)X::PA * C::RL : (uint64_t)g.P;
   const uint64_t dims[3] = {(uint64_t)g.T_pad, (uint64_t)g.cout_pad, rows};

@@ -497,13 +497,7 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   alignas(64) CUtensorMap mapV, mapU;
   if (!make_map(&mapV, V, rowsV, g.cin_pad, tc::kBM)) return NW_ERR_CUDA;
   if (!make_map(&mapU, U, rowsU, (long long)g.nsh * g.cin_pad, prm.N)) return NW_ERR_CUDA;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(tc::contraction_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
-        cudaSuccess)
-      return NW_ERR_CUDA;
-    attr = true;
-  }
+  if (ensure_smem<tc::contraction_kernel>(227 * 1024) != NW_OK) return NW_ERR_CUDA;
   int sms = 148;
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -555,12 +549,7 @@ nw_status_t launch_gemm_tc_fused(const nw_plan_st* p, const Geometry& g, const v
   if (!make_map(&mapV, V, rowsV, g.cin_pad, tc::kBM)) return NW_ERR_CUDA;
   if (!make_map(&mapU, U, rowsU, g.cin_pad, prm.N)) return NW_ERR_CUDA;
   auto kern = tc::contraction_fused_kernel<3>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
-      return NW_ERR_CUDA;
-    attr = true;
-  }
+  if (ensure_smem<tc::contraction_fused_kernel<3>>(227 * 1024) != NW_OK) return NW_ERR_CUDA;
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long units = (long long)prm.nmb * prm.PA * prm.LO;
