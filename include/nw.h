@@ -34,7 +34,8 @@
  *    channels per input-transform CTA (default 32); NW_PIPE_CHUNKS=k runs
  *    nw_conv_forward as a k-chunk three-stream pipeline (default 1) and
  *    NW_GEMM_CTAS caps its contraction grid; NW_HOST_CHUNKS=k sets the chunk
- *    count of nw_conv_forward_host (default 8).
+ *    count of nw_conv_forward_host (default 8); NW_PDL=1 launches the three hot
+ *    kernels with programmatic dependent launch.
  */
 #ifndef NW_H_
 #define NW_H_

@@ -20,6 +20,7 @@
 #pragma once
 #include <cstdlib>
 
+#include "ptx.cuh"
 #include "transforms.cuh"
 
 namespace nw {
@@ -123,6 +124,8 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
   const int aw0 = wg * C::TW;
   const int row0 = SR * (ah * X::ADV) + g.off[0];
   const int col0 = SR * (aw0 * X::ADV) + g.off[0];
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();  // x (and the workspace) may come from the previous kernel in the stream
 
   const long long pstride = (long long)g.T_pad * g.cin_pad;  // elements between consecutive points
   const long long plane = (long long)g.P * pstride;          // hi -> lo plane (bf16 elements)
@@ -273,7 +276,9 @@ static nw_status_t input_launch_c(const Geometry& g, const void* x, void* V, cud
   const long long nb = (long long)g.N * g.tiles_h * wgroups * cgroups;
   if (nb >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
   LaunchScope scope_("input_transform", s);
-  kern<<<(unsigned)nb, C::THREADS, C::SMEM, s>>>(static_cast<const XT*>(x), V, g, cgroups, wgroups);
+  if (launch_pdl(kern, dim3((unsigned)nb), dim3(C::THREADS), C::SMEM, s, static_cast<const XT*>(x), V, g, cgroups,
+                 wgroups) != NW_OK)
+    return NW_ERR_CUDA;
   return check_launch();
 }
 

@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <utility>
 #include <cstddef>
 #include <cstdint>
 
@@ -104,6 +105,26 @@ nw_status_t launch_output_transform_pre(const nw_plan_st *p, const Geometry &g, 
                                         cudaStream_t s);
 nw_status_t launch_gemm_tc(const nw_plan_st *p, const Geometry &g, const void *V, const void *U,
                            float *M, cudaStream_t s);
+
+// Launch with programmatic stream serialization (PDL): the kernel may start while the
+// previous kernel in the stream drains; it calls griddepcontrol.wait before reading
+// dependent data.  Opt-in with NW_PDL=1; otherwise a plain launch.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline nw_status_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...) == cudaSuccess ? NW_OK : NW_ERR_CUDA;
+}
 
 // RAII: when profiling is on, brackets one launch with CUDA events on its stream.
 class LaunchScope {

@@ -307,6 +307,8 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI, PRE>::THREADS, 1)
     ptx::mbar_init_fence();
   }
   __syncthreads();
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();  // M' / M comes from the contraction just before in the stream
 
   if (warp == C::WARPS) {
     // ------------------------------ TMA producer ------------------------------
@@ -364,8 +366,9 @@ static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const f
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(nunits < sms ? nunits : sms);
   LaunchScope scope_("output_transform", s);
-  kern<<<grid, C::THREADS, C::SMEM, s>>>(map, static_cast<YT*>(y), g, p->prelu ? p->slopes : nullptr, (int)nunits,
-                                         ngroups);
+  if (launch_pdl(kern, dim3(grid), dim3(C::THREADS), C::SMEM, s, map, static_cast<YT*>(y), g,
+                 p->prelu ? p->slopes : nullptr, (int)nunits, ngroups) != NW_OK)
+    return NW_ERR_CUDA;
   return check_launch();
 }
 

@@ -19,6 +19,16 @@ namespace nw {
 
 std::atomic<unsigned long long> g_launches{0};
 
+// Programmatic dependent launch is opt-in (NW_PDL=1): measured 1 % slower on C2 / C3
+// (dependent CTAs parked on SMs during the previous kernel's tail), see DESIGN.md section 5.
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("NW_PDL");
+    return v && atoi(v) == 1;
+  }();
+  return on;
+}
+
 static void phase_split(const nw_plan_st *p, int *mode, int *n_sp, int *Kp, int off[2],
                         int taps[2][kMaxTaps]) {
   const int K = p->K;

@@ -69,6 +69,13 @@ __device__ __forceinline__ long long lds_s64(uint32_t a) {
   asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(a));
   return v;
 }
+// Programmatic dependent launch: let the next kernel in the stream start its prologue, and
+// wait until the previous kernel's results are visible before touching dependent data
+// (both are no-ops for a kernel launched without the PDL attribute).
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // Give the L2 lines of [p, p + bytes) back without a write-back (the data is dead).
 __device__ __forceinline__ void discard_l2_128(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");

@@ -145,6 +145,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_launch_dependents();
+  griddep_wait();  // V comes from the input transform just before in the stream
 
   if (warp == 0) {
     if (lane == 0) {
@@ -327,6 +329,8 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_launch_dependents();
+  griddep_wait();  // V comes from the input transform just before in the stream
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------- TMA producer -------------------------
@@ -505,7 +509,8 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   if (g.gemm_ctas > 0 && g.gemm_ctas < sms) sms = g.gemm_ctas;
   const int grid = (int)(units < sms ? units : sms);
   LaunchScope scope_("contraction_tc", s);
-  tc::contraction_kernel<<<grid, tc::kThreads, smem, s>>>(mapV, mapU, prm);
+  if (launch_pdl(tc::contraction_kernel, dim3(grid), dim3(tc::kThreads), smem, s, mapV, mapU, prm) != NW_OK)
+    return NW_ERR_CUDA;
   return check_launch();
 }
 
@@ -555,7 +560,7 @@ nw_status_t launch_gemm_tc_fused(const nw_plan_st* p, const Geometry& g, const v
   const long long units = (long long)prm.nmb * prm.PA * prm.LO;
   const int grid = (int)(units < sms ? units : sms);
   LaunchScope scope_("contraction_tc", s);
-  kern<<<grid, tc::kFuseThreads, smem, s>>>(mapV, mapU, prm);
+  if (launch_pdl(kern, dim3(grid), dim3(tc::kFuseThreads), smem, s, mapV, mapU, prm) != NW_OK) return NW_ERR_CUDA;
   return check_launch();
 }
 
