@@ -42,13 +42,17 @@ struct OutCfg {
   static constexpr int CO = (SPL == 1) ? 8 : (SPL == 2 ? 6 : 3);
   static constexpr int WARPS = CO * SPL;          // consumer warps
   static constexpr int TS = 32;  // slices per unit (lanes)
-  static constexpr int NST = 4;  // ring depth (point rows)
   static constexpr int STAGE = RL * CO * TS;        // floats per ring stage
-  static constexpr int YST = TS * X::MA * QW + 1;   // floats per warp output stage
+  static constexpr int HR = (X::MA + 1) / 2;        // tile rows staged per epilogue phase (two phases)
+  static constexpr int YST = TS * HR * QW + 1;      // floats per warp output stage
   static constexpr int THREADS = (WARPS + 1) * 32;
-  static constexpr size_t RING_BYTES = (size_t)NST * STAGE * 4;
   static constexpr size_t YST_BYTES = ((size_t)WARPS * YST * 4 + 127) / 128 * 128;  // keeps sinfo 8-byte aligned
   static constexpr size_t INFO_BYTES = (size_t)WARPS * TS * 16;
+  // ring depth (point rows): as deep as shared memory allows, up to 8 -- the kernel streams M
+  // at HBM rate only with ~100 KB of loads in flight per SM
+  static constexpr size_t FREE = 225 * 1024 - 256 - YST_BYTES - INFO_BYTES;
+  static constexpr int NST = (int)(FREE / (STAGE * 4)) > 8 ? 8 : (int)(FREE / (STAGE * 4));
+  static constexpr size_t RING_BYTES = (size_t)NST * STAGE * 4;
   static constexpr size_t SMEM = 128 + RING_BYTES + YST_BYTES + INFO_BYTES + 2 * NST * 8;
 };
 
@@ -241,41 +245,48 @@ __device__ __forceinline__ void out_consume(const float* ring, uint64_t* full, u
       info[lane * 2] = b;
       info[lane * 2 + 1] = lim;
     }
-#pragma unroll
-    for (int i = 0; i < MA; ++i)
-#pragma unroll
-      for (int j = 0; j < QW; ++j) yst[lane * (MA * QW) + i * QW + j] = Y[i][j];
-    __syncwarp();
     const float slope = (slopes && coe < g.cout_e) ? slopes[g.mode == 2 ? coe % g.Cout : coe] : 0.f;
     const int qw0 = T0 * MI;  // first output column of this part
+    constexpr int HR = C::HR;
+    // two phases of HR tile rows each: half the staging buffer, twice the TMA ring depth
+#pragma unroll
+    for (int hph = 0; hph < 2; ++hph) {
+#pragma unroll
+      for (int i = 0; i < HR; ++i)
+#pragma unroll
+        for (int j = 0; j < QW; ++j)
+          if (hph * HR + i < MA) yst[lane * (HR * QW) + i * QW + j] = Y[(hph * HR + i < MA) ? hph * HR + i : 0][j];
+      __syncwarp();
 #pragma unroll 1
-    for (int jj = 0; jj < QW; ++jj) {
-      const int e = lane + 32 * jj;  // (slice s, local column ql) pairs, ql fastest
-      const int s = e / QW, ql = e - s * QW;
-      const int q_w = qw0 + ql;
-      const uint32_t ia = ptx::smem_u32(info) + (uint32_t)s * 16u;
-      const long long b = ptx::lds_s64(ia);
-      const int lim = (int)ptx::lds_s64(ia + 8);
-      const uint32_t ya = ptx::smem_u32(yst) + (uint32_t)(s * (MA * QW) + ql) * 4u;
-      const int limh = lim & 255, limw = (lim >> 8) & 255;
-      const int khi = (lim >> 16) & 3, kwi = (lim >> 18) & 3;
-      const unsigned kh = khi == 0 ? OT.keep[0] : khi == 1 ? OT.keep[1] : OT.keep[2];
-      const unsigned kw = kwi == 0 ? OT.keep[0] : kwi == 1 ? OT.keep[1] : OT.keep[2];
-      int pw = 0;
+      for (int jj = 0; jj < QW; ++jj) {
+        const int e = lane + 32 * jj;  // (slice s, local column ql) pairs, ql fastest
+        const int s = e / QW, ql = e - s * QW;
+        const int q_w = qw0 + ql;
+        const uint32_t ia = ptx::smem_u32(info) + (uint32_t)s * 16u;
+        const long long b = ptx::lds_s64(ia);
+        const int lim = (int)ptx::lds_s64(ia + 8);
+        const uint32_t ya = ptx::smem_u32(yst) + (uint32_t)(s * (HR * QW) + ql) * 4u;
+        const int limh = lim & 255, limw = (lim >> 8) & 255;
+        const int khi = (lim >> 16) & 3, kwi = (lim >> 18) & 3;
+        const unsigned kh = khi == 0 ? OT.keep[0] : khi == 1 ? OT.keep[1] : OT.keep[2];
+        const unsigned kw = kwi == 0 ? OT.keep[0] : kwi == 1 ? OT.keep[1] : OT.keep[2];
+        int pw = 0;
 #pragma unroll
-      for (int q = 0; q < MA; ++q) pw = (q_w == q) ? OT.pos[q] : pw;
-      const bool okw = b >= 0 && q_w < MA && ((kw >> q_w) & 1u) && pw < limw;
-      YT* dst = y + (b < 0 ? 0 : b) + (long long)pw * colstride;
+        for (int q = 0; q < MA; ++q) pw = (q_w == q) ? OT.pos[q] : pw;
+        const bool okw = b >= 0 && q_w < MA && ((kw >> q_w) & 1u) && pw < limw;
+        YT* dst = y + (b < 0 ? 0 : b) + (long long)pw * colstride;
 #pragma unroll
-      for (int q_h = 0; q_h < MA; ++q_h) {
-        if (okw && ((kh >> q_h) & 1u) && OT.pos[q_h] < limh) {
-          float v = ptx::lds_f32(ya + q_h * QW * 4);
-          if (slopes) v = v >= 0.f ? v : slope * v;
-          dst[(long long)OT.pos[q_h] * rowstride] = from_f<YT>(v);
+        for (int i = 0; i < HR; ++i) {
+          const int q_h = hph * HR + i;
+          if (q_h < MA && okw && ((kh >> q_h) & 1u) && OT.pos[q_h < MA ? q_h : 0] < limh) {
+            float v = ptx::lds_f32(ya + i * QW * 4);
+            if (slopes) v = v >= 0.f ? v : slope * v;
+            dst[(long long)OT.pos[q_h < MA ? q_h : 0] * rowstride] = from_f<YT>(v);
+          }
         }
       }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 
