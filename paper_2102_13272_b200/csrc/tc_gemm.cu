@@ -63,6 +63,33 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// ---- cluster helpers (CTA pairs sharing the B operand) ----
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load whose box lands at the same shared offset in every CTA of ctamask, each CTA's
+// mbarrier at `bar` receiving the bytes
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                               uint16_t ctamask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "h"(ctamask)
+      : "memory");
+}
+// tcgen05.commit arriving on the mbarrier at `bar` in every CTA of ctamask
+__device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t ctamask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   bar),
+               "h"(ctamask)
+               : "memory");
+}
+
 // UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   uint64_t d = 0;
@@ -99,6 +126,10 @@ struct Params {
   int shoff[kMaxShift];
 };
 
+// CL > 1: clusters of CL CTAs work on CL consecutive 128-slice blocks of the same point;
+// each CTA loads 1/CL of every B k-block and multicasts it to the whole cluster, and every
+// CTA's MMA completion releases the B stage in all of them (B read from L2 once per cluster).
+template <int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     contraction_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapU,
                        const Params p) {
@@ -127,12 +158,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total_units = p.P * p.ngrp;
+  const int rank = (CL > 1) ? (int)cluster_rank() : 0;
+  const int ustart = (CL > 1) ? (int)blockIdx.x / CL : (int)blockIdx.x;
+  const int ustep = (CL > 1) ? (int)gridDim.x / CL : (int)gridDim.x;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mapV);
     tma_prefetch(&mapU);
     for (int i = 0; i < p.nA; ++i) { mbar_init(smem_u32(&A_full[i]), 1); mbar_init(smem_u32(&A_empty[i]), 1); }
-    for (int i = 0; i < p.nB; ++i) { mbar_init(smem_u32(&B_full[i]), 1); mbar_init(smem_u32(&B_empty[i]), 1); }
+    for (int i = 0; i < p.nB; ++i) { mbar_init(smem_u32(&B_full[i]), 1); mbar_init(smem_u32(&B_empty[i]), CL); }
     for (int i = 0; i < 2; ++i) { mbar_init(smem_u32(&T_full[i]), 1); mbar_init(smem_u32(&T_empty[i]), 128); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -143,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   fence_before();
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync();  // every CTA's barriers are initialised before multicasts target them
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_launch_dependents();
@@ -153,10 +189,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------ TMA producer ------------------------------
       int sa = 0, sb = 0;
       uint32_t pa = 0, pb = 0;
-      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      for (int u = ustart; u < total_units; u += ustep) {
         const int xi = u / p.ngrp, grp = u % p.ngrp;
-        const int mb0 = grp * p.G;
-        const int g_eff = min(p.G, p.nmb - mb0);
+        const int mb0 = (CL > 1) ? grp * CL + rank : grp * p.G;
+        const int g_eff = (CL > 1) ? 1 : min(p.G, p.nmb - mb0);
         for (int kb = 0; kb < p.KB; ++kb) {
           mbar_wait(smem_u32(&B_empty[sb]), pb ^ 1);
           const uint32_t bfull = smem_u32(&B_full[sb]);
@@ -164,8 +200,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t bdst = base + b_off + sb * b_stage;
           const int sh = kb / p.kbc, kc = kb - sh * p.kbc;
           const int bcol = sh * p.cin_pad + kc * kBK, acol = kc * kBK, aoff = p.shoff[sh];
-          tma_load_2d(bdst, &mapU, bfull, bcol, xi * p.N);
-          if (p.lo) tma_load_2d(bdst + b_plane, &mapU, bfull, bcol, (int)(p.b_lo_row + (long long)xi * p.N));
+          if constexpr (CL > 1) {
+            const int rows = p.N / CL;  // this CTA's slice of the B tile, multicast to the cluster
+            const uint32_t so = (uint32_t)(rank * rows) * (kBK * 2);
+            tma_load_2d_mc(bdst + so, &mapU, bfull, bcol, xi * p.N + rank * rows, kMask);
+            if (p.lo)
+              tma_load_2d_mc(bdst + b_plane + so, &mapU, bfull, bcol,
+                             (int)(p.b_lo_row + (long long)xi * p.N) + rank * rows, kMask);
+          } else {
+            tma_load_2d(bdst, &mapU, bfull, bcol, xi * p.N);
+            if (p.lo) tma_load_2d(bdst + b_plane, &mapU, bfull, bcol, (int)(p.b_lo_row + (long long)xi * p.N));
+          }
           if (++sb == p.nB) { sb = 0; pb ^= 1; }
           for (int g = 0; g < g_eff; ++g) {
             mbar_wait(smem_u32(&A_empty[sa]), pa ^ 1);
@@ -194,9 +239,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int sa = 0, sb = 0;
       uint32_t pa = 0, pb = 0;
       int it = 0;
-      for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++it) {
+      for (int u = ustart; u < total_units; u += ustep, ++it) {
         const int grp = u % p.ngrp;
-        const int g_eff = min(p.G, p.nmb - grp * p.G);
+        const int g_eff = (CL > 1) ? 1 : min(p.G, p.nmb - grp * p.G);
         const int buf = it & 1;
         const uint32_t tpar = (uint32_t)((it >> 1) & 1);
         mbar_wait(smem_u32(&T_empty[buf]), tpar ^ 1);
@@ -226,7 +271,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_commit(smem_u32(&A_empty[sa]));
             if (++sa == p.nA) { sa = 0; pa ^= 1; }
           }
-          umma_commit(smem_u32(&B_empty[sb]));
+          if constexpr (CL > 1) umma_commit_mc(smem_u32(&B_empty[sb]), kMask);  // frees the stage cluster-wide
+          else umma_commit(smem_u32(&B_empty[sb]));
           if (++sb == p.nB) { sb = 0; pb ^= 1; }
         }
         umma_commit(smem_u32(&T_full[buf]));
@@ -237,10 +283,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;                     // TMEM lanes [32q, 32q+32)
     const int row = quarter * 32 + lane;
     int it = 0;
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++it) {
+    for (int u = ustart; u < total_units; u += ustep, ++it) {
       const int xi = u / p.ngrp, grp = u % p.ngrp;
-      const int mb0 = grp * p.G;
-      const int g_eff = min(p.G, p.nmb - mb0);
+      const int mb0 = (CL > 1) ? grp * CL + rank : grp * p.G;
+      // (a cluster's last group may run past the slices: its MMAs ran on zero-filled rows, nothing is stored)
+      const int g_eff = (CL > 1) ? (mb0 < p.nmb ? 1 : 0) : min(p.G, p.nmb - mb0);
       const int buf = it & 1;
       const uint32_t tpar = (uint32_t)((it >> 1) & 1);
       mbar_wait(smem_u32(&T_full[buf]), tpar);
@@ -263,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   fence_before();
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync();  // no CTA leaves while its pair may still multicast into it
   fence_after();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u));
 }
@@ -500,17 +548,44 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   if (rowsV >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
   alignas(64) CUtensorMap mapV, mapU;
   if (!make_map(&mapV, V, rowsV, g.cin_pad, tc::kBM)) return NW_ERR_CUDA;
-  if (!make_map(&mapU, U, rowsU, (long long)g.nsh * g.cin_pad, prm.N)) return NW_ERR_CUDA;
-  if (ensure_smem<tc::contraction_kernel>(227 * 1024) != NW_OK) return NW_ERR_CUDA;
+  // CTA pairs share B when one B k-block serves a single A block (N > 128) and there is more
+  // than one block per point: B is then read from L2 once per pair (NW_CLUSTER=1 disables)
+  static const int cl_env = [] {
+    const char* v = getenv("NW_CLUSTER");
+    return v ? atoi(v) : 2;
+  }();
+  const int CL = (cl_env == 2 && prm.G == 1 && prm.nmb >= 2 && g.nsh == 1 && prm.N % 16 == 0) ? 2 : 1;
+  if (CL > 1) prm.ngrp = (prm.nmb + CL - 1) / CL;
+  if (!make_map(&mapU, U, rowsU, (long long)g.nsh * g.cin_pad, prm.N / CL)) return NW_ERR_CUDA;
+  if (CL > 1 ? ensure_smem<tc::contraction_kernel<2>>(227 * 1024) != NW_OK
+             : ensure_smem<tc::contraction_kernel<1>>(227 * 1024) != NW_OK)
+    return NW_ERR_CUDA;
   int sms = 148;
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long units = (long long)prm.P * prm.ngrp;
+  const long long units = (long long)prm.P * prm.ngrp * CL;  // CTA-units
   if (g.gemm_ctas > 0 && g.gemm_ctas < sms) sms = g.gemm_ctas;
-  const int grid = (int)(units < sms ? units : sms);
+  int grid = (int)(units < sms ? units : sms);
+  grid -= grid % CL;
   LaunchScope scope_("contraction_tc", s);
-  if (launch_pdl(tc::contraction_kernel, dim3(grid), dim3(tc::kThreads), smem, s, mapV, mapU, prm) != NW_OK)
+  if (CL > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tc::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, tc::contraction_kernel<2>, mapV, mapU, prm) != cudaSuccess) return NW_ERR_CUDA;
+  } else if (launch_pdl(tc::contraction_kernel<1>, dim3(grid), dim3(tc::kThreads), smem, s, mapV, mapU, prm) !=
+             NW_OK) {
     return NW_ERR_CUDA;
+  }
   return check_launch();
 }
 

@@ -152,3 +152,12 @@ def test_table1_shapes(name, path):
     conv = NestedConv2d(t["w"].cuda(), 1, layer.pad, layer.m_o, layer.m_i, _math("bf16x3"), outer_taps=layer.r_o)
     y = conv(t["x"].cuda(), path=path).cpu().numpy()
     assert rel_err(y, _ref(layer, t)) <= TOL["bf16x3"]
+
+
+@pytest.mark.parametrize("Cout,N,H,W", [(256, 1, 40, 30), (144, 3, 37, 41), (208, 2, 50, 26)])
+def test_wide_output_cta_pairs(Cout, N, H, W):
+    # Cout_pad > 128: the contraction runs as CTA pairs that multicast the shared B (U) tile;
+    # odd 128-slice block counts leave one CTA of the last pair without a block
+    layer = synth.small(synth.CONFIGS["c3"], N=N, H=H, W=W, Cin=64, Cout=Cout)
+    t, y = _run(layer, "bf16x3")
+    assert rel_err(y, _ref(layer, t)) <= max(TOL["bf16x3"], 2.0 ** -8)
