@@ -39,8 +39,14 @@ WORKLOADS = {
     "c4": ["c4a", "c4b"],
     "c5": ["c5_conv1", "c5_deconv"],
     "table1": synth.TABLE1,
+    "c5net": synth.C5_NET,
 }
+# workloads run as one network: layer i+1 consumes layer i's output (FSRCNN-s forward);
+# layers with K <= 3 (1x1, 3x3) run the direct implicit-GEMM path of the library
+CHAINS = {"c5net"}
 WORKLOAD_DESC = {
+    "c5net": "configs[4] as a network: conv5x5 1->32 +PReLU (nested) -> 1x1 32->5 -> 3x3 5->5 -> 1x1 5->32 "
+             "(+PReLU each, direct implicit GEMM) -> 9x9 s2 deconv 32->1 (nested), N=16, 540x960 -> 1080x1920",
     "table1": "paper Table I conv2d shapes (P:154-160): SRCNN 9x9 64<-1, 5x5 32<-64, 5x5 1<-32, 256x256, N=8, fp32",
     "c1": "configs[0]: 5x5 s1 p2, N=1, Cin=Cout=16, 32x32, fp32, F(2,3)(x)F(2,3) + coverage phases",
     "c2": "configs[1]: filter-size sweep K in {5,7,9}, s1 same pad, N=32, Cin=Cout=64, 128x128, fp32",
@@ -56,7 +62,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=list(WORKLOADS))
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "table1", "c5net"])
     ap.add_argument("--math", default="bf16x3", choices=["bf16x3", "fp32", "bf16"])
     ap.add_argument("--path", default="nested", choices=["nested", "ola", "direct"])
     ap.add_argument("--m-outer", type=int, default=None,
@@ -137,9 +143,28 @@ def load_peaks():
 # ----------------------------------------------------------------------------
 # algorithmic work per launch of each kernel kind
 # ----------------------------------------------------------------------------
-def kernel_work(layer, info, math):
+def kernel_work(layer, info, math, path="nested"):
     """Algorithmic bytes and flops of one launch of each kernel for one layer."""
     es = 2 if layer.dtype == "bf16" else 4
+    if path == "direct":
+        # implicit GEMM over the (phase) pixel grid extended by Kp - 1 (DESIGN.md section 1, a5)
+        Kp = info["Kp"]
+        if layer.transposed:
+            Hq, Wq = -(-layer.Ho // 2), -(-layer.Wo // 2)
+        else:
+            Hq, Wq = layer.Ho, layer.Wo
+        T = layer.N * (Hq + Kp - 1) * (Wq + Kp - 1)
+        x_b = layer.N * layer.Cin * layer.H * layer.W * es
+        y_b = layer.N * layer.Cout * layer.Ho * layer.Wo * es
+        v_b, m_b = T * info["cin_e"] * 4, T * info["cout_e"] * 4
+        u_b = Kp * Kp * info["cout_e"] * info["cin_e"] * 4
+        passes = {"bf16x3": 3, "bf16": 1, "fp32": 1}[math]
+        flops = 2 * T * Kp * Kp * info["cin_e"] * info["cout_e"]
+        return {"pack_input": {"bytes": x_b + v_b, "flops": 0},
+                "contraction_tc": {"bytes": v_b + u_b + m_b, "flops": flops * passes},
+                "contraction_fp32_simt": {"bytes": v_b + u_b + m_b, "flops": flops},
+                "unpack_output": {"bytes": m_b + y_b, "flops": 0},
+                "filter_transform": {"bytes": u_b, "flops": 0}}
     P = info["points"]
     adv, nph = info["tile_out"], info["n_phase"]
     if layer.transposed:
@@ -170,8 +195,9 @@ def roofline(prof, works, math, peaks, steps, layers):
         return None
     kind = max(prof, key=lambda k: prof[k][1])
     launches, ms = prof[kind]
-    bytes_per_launch = sum(w[kind]["bytes"] for w in works) / len(works)
-    flops_per_launch = sum(w[kind]["flops"] for w in works) / len(works)
+    ws_ = [w for w in works if kind in w]          # layers that launch this kernel (once per step each)
+    bytes_per_launch = sum(w[kind]["bytes"] for w in ws_) / len(ws_)
+    flops_per_launch = sum(w[kind]["flops"] for w in ws_) / len(ws_)
     avg_s = ms / launches / 1e3
     hbm = peaks["hbm_gbs"]
     if kind == "contraction_tc":
@@ -271,10 +297,14 @@ def main():
     peaks = load_peaks()
     stream = torch.cuda.current_stream()
 
+    chain = args.workload in CHAINS
+    paths = [("direct" if (chain and l.K <= 3) else args.path) for l in layers_all]
     convs, xs, ys, works = [], [], [], []
     filt_ms = 0.0
-    for l in layers_all:
+    for li, l in enumerate(layers_all):
         t = synth.make_inputs(l.with_(seed=l.seed + 1000 * rank)) if rank else synth.make_inputs(l)
+        if chain and li > 0:
+            t["x"] = None                                   # consumes the previous layer's output
         w = synth.make_inputs(l, x=False)["w"].to(dev)     # same weights on every rank
         slopes = torch.full((l.Cout,), synth.PRELU_SLOPE, device=dev) if l.prelu else None
         conv = nw.NestedConv2d(w, l.stride, l.pad, l.m_o, l.m_i, math, transposed=l.transposed, outer_taps=l.r_o,
@@ -287,19 +317,19 @@ def main():
         torch.cuda.synchronize()
         filt_ms += e0.elapsed_time(e1)
         nwd.broadcast_filter(conv.U, src=0)   # the one collective: U from rank 0 (NCCL / NVLink)
-        x = t["x"].to(dev)
+        x = ys[-1] if (chain and li > 0) else t["x"].to(dev)
         y = torch.empty(conv.out_shape(x.shape), dtype=x.dtype, device=dev)
-        conv.workspace(*x.shape[:1], *x.shape[2:], path=args.path)
+        conv.workspace(*x.shape[:1], *x.shape[2:], path=paths[li])
         convs.append(conv)
         xs.append(x)
         ys.append(y)
-        works.append(kernel_work(l, conv.info, args.math))
+        works.append(kernel_work(l, conv.info, args.math, paths[li]))
         del t
     torch.cuda.synchronize()
 
     def step():
-        for conv, x, y in zip(convs, xs, ys):
-            conv(x, y, path=args.path)
+        for conv, x, y, pth in zip(convs, xs, ys, paths):
+            conv(x, y, path=pth)
 
     for _ in range(args.warmup):
         step()
@@ -333,16 +363,17 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = max(3, args.steps // 2)
         e0.record()
+        pth = paths[len(per_layer)]
         for _ in range(reps):
-            conv(x, y, path=args.path)
+            conv(x, y, path=pth)
         e1.record()
         torch.cuda.synchronize()
         lm = e0.elapsed_time(e1) / reps
-        per_layer.append({"layer": l.name, "ms": round(lm, 4),
+        per_layer.append({"layer": l.name, "path": pth, "ms": round(lm, 4),
                           "tflops_direct_equiv": round(l.direct_flops() / (lm / 1e3) / 1e12, 2)})
 
     compare = {}
-    if not args.no_compare and args.path == "nested":
+    if not args.no_compare and args.path == "nested" and not chain:
         for path in ("ola", "direct"):
             try:
                 tot = 0.0
@@ -373,7 +404,34 @@ def main():
 
     # e2e: same metric through the C ABI with host buffers (copies inside the timed region)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and chain:
+        # network forward end to end: pinned host input -> device, the layer chain through the
+        # C ABI, last output -> pinned host; copies inside the timed region
+        hx0 = xs[0].cpu().pin_memory()
+        hyl = torch.empty(ys[-1].shape, dtype=ys[-1].dtype).pin_memory()
+
+        def e2e_chain():
+            xs[0].copy_(hx0, non_blocking=True)
+            step()
+            hyl.copy_(ys[-1], non_blocking=True)
+
+        for _ in range(2):
+            e2e_chain()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ek = max(3, args.steps // 4)
+        s0.record(stream)
+        for _ in range(ek):
+            e2e_chain()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        ems = nwd.max_over_ranks(s0.elapsed_time(s1) / ek, dev)
+        e2e = {"value": round(flops_rank * world / (ems / 1e3) / 1e12, 3), "unit": "TFLOP/s",
+               "ms_per_step": round(ems, 3), "h2d_bytes_per_step": int(hx0.numel() * hx0.element_size()),
+               "d2h_bytes_per_step": int(hyl.numel() * hyl.element_size())}
+    elif not args.no_e2e:
         hx = [x.cpu().pin_memory() for x in xs]
         hy = [torch.empty(y.shape, dtype=y.dtype).pin_memory() for y in ys]
         wss = []
@@ -424,7 +482,8 @@ def main():
             "config": {"workload": WORKLOAD_DESC[args.workload], "layers": [l.name for l in layers_all],
                        "nesting": [f"F({c.info['m_outer']},{c.info['r_outer']})(x)F({c.info['m_inner']},3)"
                                    for c in convs],
-                       "path": args.path, "math": args.math, "images_per_rank": layers_all[0].N,
+                       "path": paths if chain else args.path, "math": args.math,
+                       "images_per_rank": layers_all[0].N,
                        "l2": "no flush: x (>=134 MB) and V/M (>1 GB per layer) exceed the 126 MB L2",
                        "step": "input transform + contraction + output transform per layer (nw_conv_forward)"},
             "images_per_s": round(images, 1),
