@@ -100,6 +100,18 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= (uint64_t)2 << 61;                           // layout: SWIZZLE_128B
   return d;
 }
+// K-major descriptor for a K block of kbk bf16 (rows of 2*kbk bytes, swizzle span = row):
+// kbk 64 -> SWIZZLE_128B, 32 -> SWIZZLE_64B, 16 -> SWIZZLE_32B; 8-row groups 16*kbk bytes apart.
+// Narrow K blocks serve layers with 16 / 32 contraction channels without zero-padding to 64.
+__device__ __forceinline__ uint64_t swk_desc(uint32_t saddr, int kbk) {
+  const uint32_t layout = kbk == 64 ? 2u : (kbk == 32 ? 4u : 6u);
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(((16u * (uint32_t)kbk) >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
+  return d;
+}
 // Instruction descriptor: D fp32, A/B bf16, both K-major, M=128, N=n.
 __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
@@ -123,6 +135,7 @@ struct Params {
   // shift s = kb / kbc and channel block kc = kb % kbc; its A rows are read at
   // t + shoff[s] and its B columns at s * cin_pad + kc * 64.  Nested: nsh = 1.
   int nsh, kbc, cin_pad;
+  int kbk;           // K block width in bf16 elements (64, 32 or 16)
   int shoff[kMaxShift];
 };
 
@@ -139,9 +152,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* sbase = smem_raw + (base - raw);
 
-  const uint32_t a_plane = kBM * kBK * 2;              // 16 KB
+  const uint32_t a_plane = kBM * p.kbk * 2;            // 16 KB at kbk 64
   const uint32_t a_stage = a_plane * (p.lo ? 2 : 1);
-  const uint32_t b_plane = (uint32_t)p.N * kBK * 2;    // N x 128 B
+  const uint32_t b_plane = (uint32_t)p.N * p.kbk * 2;  // N rows of 2 kbk bytes
   const uint32_t b_stage = b_plane * (p.lo ? 2 : 1);
   const uint32_t a_off = 0;
   const uint32_t b_off = a_off + a_stage * p.nA;
@@ -199,10 +212,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(bfull, b_stage);
           const uint32_t bdst = base + b_off + sb * b_stage;
           const int sh = kb / p.kbc, kc = kb - sh * p.kbc;
-          const int bcol = sh * p.cin_pad + kc * kBK, acol = kc * kBK, aoff = p.shoff[sh];
+          const int bcol = sh * p.cin_pad + kc * p.kbk, acol = kc * p.kbk, aoff = p.shoff[sh];
           if constexpr (CL > 1) {
             const int rows = p.N / CL;  // this CTA's slice of the B tile, multicast to the cluster
-            const uint32_t so = (uint32_t)(rank * rows) * (kBK * 2);
+            const uint32_t so = (uint32_t)(rank * rows) * (p.kbk * 2);
             tma_load_2d_mc(bdst + so, &mapU, bfull, bcol, xi * p.N + rank * rows, kMask);
             if (p.lo)
               tma_load_2d_mc(bdst + b_plane + so, &mapU, bfull, bcol,
@@ -256,14 +269,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t asm_ = base + a_off + sa * a_stage;
             const uint32_t acc = acc0 + (uint32_t)(g * p.N);
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) {
-              const uint64_t ah = sw128_desc(asm_ + k * 32);
-              const uint64_t bh = sw128_desc(bsm + k * 32);
+            for (int k = 0; k < p.kbk / 16; ++k) {
+              const uint64_t ah = swk_desc(asm_ + k * 32, p.kbk);
+              const uint64_t bh = swk_desc(bsm + k * 32, p.kbk);
               const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
               umma_f16(acc, ah, bh, idesc, accum);
               if (p.lo) {
-                const uint64_t al = sw128_desc(asm_ + a_plane + k * 32);
-                const uint64_t bl = sw128_desc(bsm + b_plane + k * 32);
+                const uint64_t al = swk_desc(asm_ + a_plane + k * 32, p.kbk);
+                const uint64_t bl = swk_desc(bsm + b_plane + k * 32, p.kbk);
                 umma_f16(acc, ah, bl, idesc, 1u);
                 umma_f16(acc, al, bh, idesc, 1u);
               }
@@ -331,6 +344,7 @@ constexpr int kSlots = 8;
 
 struct FusedParams {
   int nmb, N, KB, lo, nst;
+  int kbk;                // K block width in bf16 elements (64, 32 or 16)
   int PA, LO;             // points per axis, outer points per axis
   long long T_pad;
   long long a_lo_row, b_lo_row;
@@ -348,7 +362,7 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* sbase = smem_raw + (base - raw);
-  const uint32_t a_plane = kBM * kBK * 2, b_plane = (uint32_t)p.N * kBK * 2;
+  const uint32_t a_plane = kBM * p.kbk * 2, b_plane = (uint32_t)p.N * p.kbk * 2;
   const uint32_t a_bytes = a_plane * (p.lo ? 2 : 1), b_bytes = b_plane * (p.lo ? 2 : 1);
   const uint32_t stage = a_bytes + b_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + (size_t)stage * p.nst);
@@ -402,10 +416,11 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
               row = (long long)xi * p.T_pad + (long long)mb * kBM;
               lrow = p.a_lo_row + row;
             }
-            tma_load_2d(dst, &mapV, fb, kb * kBK, (int)row);
-            if (p.lo) tma_load_2d(dst + a_plane, &mapV, fb, kb * kBK, (int)lrow);
-            tma_load_2d(dst + a_bytes, &mapU, fb, kb * kBK, xi * p.N);
-            if (p.lo) tma_load_2d(dst + a_bytes + b_plane, &mapU, fb, kb * kBK, (int)(p.b_lo_row + (long long)xi * p.N));
+            tma_load_2d(dst, &mapV, fb, kb * p.kbk, (int)row);
+            if (p.lo) tma_load_2d(dst + a_plane, &mapV, fb, kb * p.kbk, (int)lrow);
+            tma_load_2d(dst + a_bytes, &mapU, fb, kb * p.kbk, xi * p.N);
+            if (p.lo)
+              tma_load_2d(dst + a_bytes + b_plane, &mapU, fb, kb * p.kbk, (int)(p.b_lo_row + (long long)xi * p.N));
             if (++st == p.nst) { st = 0; ph ^= 1; }
           }
         }
@@ -428,12 +443,12 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
             fence_after();
             const uint32_t asm_ = base + (uint32_t)st * stage, bsm = asm_ + a_bytes;
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) {
-              const uint64_t ah = sw128_desc(asm_ + k * 32), bh = sw128_desc(bsm + k * 32);
+            for (int k = 0; k < p.kbk / 16; ++k) {
+              const uint64_t ah = swk_desc(asm_ + k * 32, p.kbk), bh = swk_desc(bsm + k * 32, p.kbk);
               umma_f16(acc, ah, bh, idesc, (kb > 0 || k > 0) ? 1u : 0u);
               if (p.lo) {
-                umma_f16(acc, ah, sw128_desc(bsm + b_plane + k * 32), idesc, 1u);
-                umma_f16(acc, sw128_desc(asm_ + a_plane + k * 32), bh, idesc, 1u);
+                umma_f16(acc, ah, swk_desc(bsm + b_plane + k * 32, p.kbk), idesc, 1u);
+                umma_f16(acc, swk_desc(asm_ + a_plane + k * 32, p.kbk), bh, idesc, 1u);
               }
             }
             umma_commit(smem_u32(&empty[st]));
@@ -499,11 +514,24 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
 
 // ------------------------------ host side ------------------------------------
 // 2-D bf16 tensor map [rows][cols] with a (64 x box_rows) box, 128-byte swizzle.
-static bool make_map(CUtensorMap* m, const void* base, long long rows, long long cols, int box_rows) {
+static bool make_map(CUtensorMap* m, const void* base, long long rows, long long cols, int box_rows, int kbk = 64) {
   const uint64_t dims[2] = {(uint64_t)cols, (uint64_t)rows};
   const uint64_t strides[1] = {(uint64_t)cols * 2};
-  const uint32_t box[2] = {(uint32_t)tc::kBK, (uint32_t)box_rows};
-  return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  const uint32_t box[2] = {(uint32_t)kbk, (uint32_t)box_rows};
+  const CUtensorMapSwizzle sw =
+      kbk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : (kbk == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, sw);
+}
+
+// K block width: the whole contraction channel pitch when it is 16 or 32 (no zero padding to
+// 64 in the MMA K loop), else 64.  NW_KBK=64 forces the wide block.
+static int pick_kbk(int cin_pad) {
+  static const int force = [] {
+    const char* v = getenv("NW_KBK");
+    return v ? atoi(v) : 0;
+  }();
+  if (force == 64) return 64;
+  return (cin_pad == 16 || cin_pad == 32) ? cin_pad : 64;
 }
 
 nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V, const void* U, float* M,
@@ -519,7 +547,8 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   prm.ngrp = (prm.nmb + prm.G - 1) / prm.G;
   if (g.nsh < 1 || g.nsh > kMaxShift) return NW_ERR_UNSUPPORTED;
   prm.nsh = g.nsh;
-  prm.kbc = (g.cin_pad + tc::kBK - 1) / tc::kBK;
+  prm.kbk = pick_kbk(g.cin_pad);
+  prm.kbc = (g.cin_pad + prm.kbk - 1) / prm.kbk;
   prm.cin_pad = g.cin_pad;
   prm.KB = prm.nsh * prm.kbc;
   for (int b = 0; b < g.nsh; ++b) prm.shoff[b] = (b / g.nb) * g.tiles_w + (b % g.nb);  // Eq. 2.3 block shift
@@ -529,8 +558,8 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   prm.b_lo_row = (long long)g.P * g.cout_pad;
   prm.vblk = (g.vblk && prm.lo) ? 1 : 0;
   prm.M = M;
-  const uint32_t a_stage = tc::kBM * tc::kBK * 2 * (prm.lo ? 2 : 1);
-  const uint32_t b_stage = (uint32_t)prm.N * tc::kBK * 2 * (prm.lo ? 2 : 1);
+  const uint32_t a_stage = tc::kBM * prm.kbk * 2 * (prm.lo ? 2 : 1);
+  const uint32_t b_stage = (uint32_t)prm.N * prm.kbk * 2 * (prm.lo ? 2 : 1);
   // ring depths within ~200 KB
   const uint32_t budget = 200 * 1024;
   prm.nB = 2;
@@ -547,7 +576,7 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   const long long rowsU = (long long)g.P * g.cout_pad * (prm.lo ? 2 : 1);
   if (rowsV >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
   alignas(64) CUtensorMap mapV, mapU;
-  if (!make_map(&mapV, V, rowsV, g.cin_pad, tc::kBM)) return NW_ERR_CUDA;
+  if (!make_map(&mapV, V, rowsV, g.cin_pad, tc::kBM, prm.kbk)) return NW_ERR_CUDA;
   // CTA pairs share B when one B k-block serves a single A block (N > 128) and there is more
   // than one block per point: B is then read from L2 once per pair (NW_CLUSTER=1 disables)
   static const int cl_env = [] {
@@ -556,7 +585,7 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   }();
   const int CL = (cl_env == 2 && prm.G == 1 && prm.nmb >= 2 && g.nsh == 1 && prm.N % 16 == 0) ? 2 : 1;
   if (CL > 1) prm.ngrp = (prm.nmb + CL - 1) / CL;
-  if (!make_map(&mapU, U, rowsU, (long long)g.nsh * g.cin_pad, prm.N / CL)) return NW_ERR_CUDA;
+  if (!make_map(&mapU, U, rowsU, (long long)g.nsh * g.cin_pad, prm.N / CL, prm.kbk)) return NW_ERR_CUDA;
   if (CL > 1 ? ensure_smem<tc::contraction_kernel<2>>(227 * 1024) != NW_OK
              : ensure_smem<tc::contraction_kernel<1>>(227 * 1024) != NW_OK)
     return NW_ERR_CUDA;
@@ -606,7 +635,8 @@ nw_status_t launch_gemm_tc_fused(const nw_plan_st* p, const Geometry& g, const v
   tc::FusedParams prm{};
   prm.nmb = (int)(g.T_pad / tc::kBM);
   prm.N = g.cout_pad;
-  prm.KB = (g.cin_pad + tc::kBK - 1) / tc::kBK;
+  prm.kbk = pick_kbk(g.cin_pad);
+  prm.KB = (g.cin_pad + prm.kbk - 1) / prm.kbk;
   prm.lo = (p->math == NW_MATH_BF16X3) ? 1 : 0;
   const NestedAxis ax = path_axis(p, g.path);
   prm.PA = ax.Pa;
@@ -617,7 +647,7 @@ nw_status_t launch_gemm_tc_fused(const nw_plan_st* p, const Geometry& g, const v
   prm.P = g.P;
   prm.vblk = (g.vblk && prm.lo) ? 1 : 0;
   prm.Mp = Mp;
-  const uint32_t stage = (tc::kBM * tc::kBK * 2 + (uint32_t)prm.N * tc::kBK * 2) * (prm.lo ? 2 : 1);
+  const uint32_t stage = (tc::kBM * prm.kbk * 2 + (uint32_t)prm.N * prm.kbk * 2) * (prm.lo ? 2 : 1);
   prm.nst = (int)((200u * 1024u) / stage);
   if (prm.nst > tc::kMaxStages) prm.nst = tc::kMaxStages;
   if (prm.nst < 2) return NW_ERR_UNSUPPORTED;
@@ -626,8 +656,8 @@ nw_status_t launch_gemm_tc_fused(const nw_plan_st* p, const Geometry& g, const v
   const long long rowsU = (long long)g.P * g.cout_pad * (prm.lo ? 2 : 1);
   if (rowsV >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
   alignas(64) CUtensorMap mapV, mapU;
-  if (!make_map(&mapV, V, rowsV, g.cin_pad, tc::kBM)) return NW_ERR_CUDA;
-  if (!make_map(&mapU, U, rowsU, g.cin_pad, prm.N)) return NW_ERR_CUDA;
+  if (!make_map(&mapV, V, rowsV, g.cin_pad, tc::kBM, prm.kbk)) return NW_ERR_CUDA;
+  if (!make_map(&mapU, U, rowsU, g.cin_pad, prm.N, prm.kbk)) return NW_ERR_CUDA;
   auto kern = tc::contraction_fused_kernel<3>;
   if (ensure_smem<tc::contraction_fused_kernel<3>>(227 * 1024) != NW_OK) return NW_ERR_CUDA;
   int sms = 148, dev = 0;
