@@ -74,7 +74,7 @@ CONFIGS: Dict[str, Layer] = {
     "c3": Layer("c3", 64, 256, 256, 64, 64, 9, 1, 4, m_o=4, dtype="bf16", xdist="relu_normal", seed=3),
     # configs[3]: strided large filters (stride-Winograd phases)
     "c4a": Layer("c4a", 256, 3, 64, 224, 224, 7, 2, 3, m_o=4, r_o=0, xdist="unif01", seed=41),
-    "c4b": Layer("c4b", 256, 64, 64, 112, 112, 9, 2, 4, m_o=4, xdist="unif01", seed=42),
+    "c4b": Layer("c4b", 256, 64, 64, 112, 112, 9, 2, 4, m_o=4, r_o=0, xdist="unif01", seed=42),
     # configs[4]: FSRCNN-s shaped network, nested layers first and last
     "c5_conv1": Layer("c5_conv1", 16, 1, 32, 540, 960, 5, 1, 2, m_o=4, r_o=0, xdist="unif01", seed=5,
                       prelu=True),
@@ -82,7 +82,7 @@ CONFIGS: Dict[str, Layer] = {
     "c5_conv3": Layer("c5_conv3", 16, 5, 5, 540, 960, 3, 1, 1, seed=52, prelu=True),
     "c5_conv4": Layer("c5_conv4", 16, 5, 32, 540, 960, 1, 1, 0, seed=53, prelu=True),
     "c5_deconv": Layer("c5_deconv", 16, 32, 1, 540, 960, 9, 2, 4, transposed=True, output_padding=1,
-                       m_o=4, seed=54),
+                       m_o=4, r_o=0, seed=54),
 }
 
 # Table I of the paper (ZCU102): the conv2d layer shapes (Cout, Cin, H, W), measured
