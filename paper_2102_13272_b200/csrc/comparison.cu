@@ -38,10 +38,15 @@ __global__ void __launch_bounds__(256) pack_input_kernel(const XT* __restrict__ 
     const int j = i % 32, ce = i / 32;
     const int v = v0 + j;
     int ci = ce, p = 0, q = 0;
-    if (g.mode == 1) { ci = ce / 4; p = (ce % 4) / 2; q = ce % 2; }
+    if (g.mode == 1) {  // phase-major stride-2 channels: ce = (2p + q) * cs + ci
+      const int phase = ce / g.cs;
+      ci = phase < 4 ? ce - phase * g.cs : g.Cin;
+      p = phase / 2;
+      q = phase % 2;
+    }
     const int r = g.SR * u + p + g.off[0], c = g.SR * v + q + g.off[0];
     float val = 0.f;
-    if (v < g.tiles_w && ci < g.Cin && ce < g.cin_e && r >= 0 && r < g.H && c >= 0 && c < g.W)
+    if (v < g.tiles_w && ci < g.Cin && r >= 0 && r < g.H && c >= 0 && c < g.W)
       val = to_f(x[(((long long)n * g.Cin + ci) * g.H + r) * g.W + c]);
     sm[j * cs + ce] = val;
   }

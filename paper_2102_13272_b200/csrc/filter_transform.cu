@@ -39,9 +39,16 @@ __global__ void __launch_bounds__(128) filter_transform_kernel(const WT* __restr
   const int R = G.R, Pa = G.Pa;
   double We[kMaxR * kMaxR];
   for (int i = 0; i < R * R; ++i) We[i] = 0.0;
-  if (ce < g.cin_e && coe < g.cout_e) {
-    int ci = ce, co = coe, ph = 0, pw = 0;
-    if (g.mode == 1) { ci = ce / 4; ph = (ce % 4) / 2; pw = ce % 2; }
+  int ci = ce, ph = 0, pw = 0;
+  if (g.mode == 1) {  // phase-major stride-2 channels: ce = (2 ph + pw) * cs + ci
+    const int phase = ce / g.cs;
+    ci = ce - phase * g.cs;
+    ph = phase / 2;
+    pw = phase % 2;
+    if (phase >= 4) ci = g.Cin;  // padding channel
+  }
+  if (ci < g.Cin && ce < g.cin_pad && coe < g.cout_e) {
+    int co = coe;
     if (g.mode == 2) { const int f = coe / g.Cout; co = coe % g.Cout; ph = f / 2; pw = f % 2; }
     for (int a = 0; a < R; ++a)
       for (int b = 0; b < R; ++b) {

@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
   __syncthreads();
 
   // ---------------- pass 2: rows along w, split, store V ----------------
-  constexpr int NPR = (SR == 1) ? CC / 2 : CC;  // channel pairs (stride 1) / channels with both column phases
+  // channel pairs; stride 2: pairs of each column phase q (phase-major ce = (2p + q) * cs + ci)
+  constexpr int NPR = (SR == 1) ? CC / 2 : CC;
   constexpr int NTASK = NPH * NPH * PA * C::TW * NPR;
 #pragma unroll 1
   for (int task = tid; task < NTASK; task += C::THREADS) {
@@ -227,13 +228,14 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
       c0 = 2 * pr; c1 = c0 + 1; q0 = q1 = 0;
       ce = cin0 + c0;
     } else {
-      c0 = c1 = pr; q0 = 0; q1 = 1;
-      ce = (cin0 + pr) * 4 + p * 2;
+      const int q = pr / (CC / 2), cp = pr - q * (CC / 2);
+      c0 = 2 * cp; c1 = c0 + 1; q0 = q1 = q;
+      ce = (p * 2 + q) * g.cs + cin0 + c0;
     }
     const float* h0 = Hs + ((phh * PA + p_h) * CC + c0) * C::CSTR;
     const float* h1 = Hs + ((phh * PA + p_h) * CC + c1) * C::CSTR;
     const int cb = tile * X::ADV + (pw == 0 ? 0 : SH1);
-    if (aw >= g.tiles_w || ce >= g.cin_pad) continue;
+    if (aw >= g.tiles_w || ce >= g.cin_pad || (SR == 2 && cin0 + c0 >= g.cs)) continue;
     float za[X::LO][X::LI], zb[X::LO][X::LI];
     {
       float a[L], bb[L];
@@ -271,7 +273,7 @@ static nw_status_t input_launch_c(const Geometry& g, const void* x, void* V, cud
   auto kern = input_transform_kernel<MO, RO, MI, SR, CC, XT, BF, CINP>;
   if (ensure_smem<input_transform_kernel<MO, RO, MI, SR, CC, XT, BF, CINP>>((int)C::SMEM) != NW_OK) return NW_ERR_CUDA;
   const int wgroups = (g.tiles_w + C::TW - 1) / C::TW;
-  const int cin_src = (SR == 1) ? g.cin_pad : g.cin_pad / 4;
+  const int cin_src = (SR == 1) ? g.cin_pad : g.cs;
   const int cgroups = (cin_src + CC - 1) / CC;
   const long long nb = (long long)g.N * g.tiles_h * wgroups * cgroups;
   if (nb >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
@@ -301,7 +303,7 @@ static nw_status_t input_pick(const Geometry& g, const void* x, void* V, cudaStr
     return v ? atoi(v) : 32;
   }();
   if (SR == 2) {  // 4 contraction channels per source channel; narrow layers (C4a: 3) take 8-channel CTAs
-    if (g.cin_pad / 4 <= 8) return input_launch<MO, RO, MI, SR, 8, XT, BF>(g, x, V, s);
+    if (g.cs <= 8) return input_launch<MO, RO, MI, SR, 8, XT, BF>(g, x, V, s);
     return input_launch<MO, RO, MI, SR, 16, XT, BF>(g, x, V, s);
   }
   if (Ax<MO, RO, MI>::NPH == 1) {

@@ -43,6 +43,7 @@ struct Geometry {
   int nsh;           // nb^2: contraction K = nsh * cin_pad, A rows shifted per block
   int gemm_ctas;     // persistent contraction grid (0: one CTA per SM)
   int vblk;          // V in the blocked split layout [T_pad/128][P][hi, lo][128][cin_pad] (nested, bf16x3)
+  int cs;            // stride 2: ce = (2p + q) * cs + ci (phase-major contraction channels)
 };
 
 constexpr int kPathNested = 0, kPathOla = 1, kPathDirect = 2;
@@ -59,6 +60,7 @@ struct nw_plan_st {
   bool finalized = false;
   // derived at finalize
   int Kp = 0, r_o = 0, cin_e = 0, cout_e = 0, cin_pad = 0, cout_pad = 0;
+  int cs = 0;  // per-phase channel stride of the stride-2 contraction channels (Cin rounded up to 4)
   nw::NestedAxis ax{};
   // copy streams of nw_conv_forward_host (created on first use, released by nw_plan_destroy)
   std::mutex io_mu;

@@ -92,7 +92,11 @@ nw_status_t finalize(nw_plan_st *p) {
   p->ax = make_axis(p->m_o, p->r_o, p->m_i);
   p->cin_e = p->Cin * ((mode == 1) ? 4 : 1);
   p->cout_e = p->Cout * ((mode == 2) ? 4 : 1);
-  p->cin_pad = (int)round_up(p->cin_e, kGranule);
+  // stride 2: contraction channels are phase-major, ce = (2p + q) * cs + ci, with the per-phase
+  // stride cs = Cin rounded up to a multiple of 4: channel pairs never straddle two phases and
+  // 4 cs is already a multiple of the 16-channel granule (every channel is written)
+  p->cs = (mode == 1) ? (int)round_up(p->Cin, 4) : p->Cin;
+  p->cin_pad = (int)round_up((mode == 1) ? 4 * p->cs : p->cin_e, kGranule);
   p->cout_pad = (int)round_up(p->cout_e, kGranule);
   if (p->prelu && !p->slopes) return NW_ERR_INVALID;
   p->finalized = true;
@@ -160,6 +164,7 @@ Geometry make_geometry(const nw_plan_st *p, int N, int H, int W, int path) {
   g.T = (long long)N * g.tiles_h * g.tiles_w * g.nph * g.nph;
   g.T_pad = round_up(g.T, 128);
   g.cin_e = p->cin_e; g.cout_e = p->cout_e;
+  g.cs = p->cs;
   g.cin_pad = p->cin_pad; g.cout_pad = p->cout_pad;
   g.Pa = ax.Pa;
   g.P = g.Pa * g.Pa;

@@ -32,4 +32,12 @@ for name in sys.argv[1:]:
     ms = e0.elapsed_time(e1) / R
     tot += ms
     print(f"{name}: {ms:.4f} ms  {l.direct_flops() / ms / 1e9:.1f} TFLOP/s")
+    if os.environ.get("KERNELS"):
+        from paper_2102_13272_b200 import _lib
+        _lib.profile_begin()
+        for _ in range(5):
+            conv(x, y)
+        torch.cuda.synchronize()
+        prof = _lib.profile_end()
+        print("   ", {k: round(v[1] / v[0], 4) for k, v in prof.items()})
 print(f"total {tot:.4f} ms")
