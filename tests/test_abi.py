@@ -124,3 +124,28 @@ def test_m_rows_reports_fused_inner_output_level():
         l_o = m_o + 2
         assert inf["m_rows"] in (inf["points"], inf["points_axis"] * l_o * 3)
     assert _lib.Plan(9, 1, 4, 3, 64, 64, math=_lib.MATH_FP32_SIMT).info()["m_rows"] == 900
+
+
+def test_forward_argument_errors_without_touching_memory():
+    # argument validation happens before any CUDA call: fake (never dereferenced) pointers suffice
+    lib = _lib.load()
+    p = _lib.Plan(9, 1, 3, 3, 16, 16)
+    FAKE = 1 << 20          # 16-byte aligned, never dereferenced
+    ws_need = p.workspace_size(2, 20, 20)
+    fwd = lib.nw_conv_forward
+    assert fwd(p.handle, FAKE, FAKE, FAKE, 0, 20, 20, FAKE, ws_need, None) == _lib.NW_ERR_INVALID   # empty batch
+    assert fwd(p.handle, FAKE, FAKE, FAKE, 2, 0, 20, FAKE, ws_need, None) == _lib.NW_ERR_INVALID   # empty image
+    assert fwd(p.handle, 0, FAKE, FAKE, 2, 20, 20, FAKE, ws_need, None) == _lib.NW_ERR_INVALID     # null x
+    assert fwd(p.handle, FAKE + 4, FAKE, FAKE, 2, 20, 20, FAKE, ws_need, None) == _lib.NW_ERR_INVALID  # misaligned
+    assert fwd(p.handle, FAKE, FAKE, FAKE, 2, 20, 20, FAKE, ws_need - 1, None) == _lib.NW_ERR_WORKSPACE
+    assert fwd(p.handle, FAKE, FAKE, FAKE, 2, 20, 20, 0, ws_need, None) == _lib.NW_ERR_WORKSPACE
+    q = _lib.Plan(9, 1, 3, 3, 16, 16, pad=0)
+    # 9x9 filter, no padding, 5x5 image: no output
+    assert lib.nw_conv_forward(q.handle, FAKE, FAKE, FAKE, 1, 5, 5, FAKE, 1 << 30, None) == _lib.NW_ERR_INVALID
+    # an outer kernel with no compiled transform (F(6,3) (x) F(3,3)) is refused, not emulated
+    r = _lib.Plan(9, 1, 6, 3, 16, 16)
+    need = r.workspace_size(1, 30, 30)
+    assert lib.nw_conv_forward(r.handle, FAKE, FAKE, FAKE, 1, 30, 30, FAKE, need, None) == _lib.NW_ERR_UNSUPPORTED
+    # comparison paths validate the same way
+    assert lib.nw_conv_ola(p.handle, FAKE, FAKE, FAKE, 0, 20, 20, FAKE, 1 << 30, None) == _lib.NW_ERR_INVALID
+    assert lib.nw_conv_direct(p.handle, FAKE, FAKE, FAKE, 2, 20, 20, FAKE, 16, None) == _lib.NW_ERR_WORKSPACE
