@@ -58,6 +58,14 @@ static nw_status_t forward_one(const nw_plan_st *p, const Geometry &g, const voi
                                float *M, cudaStream_t si, cudaStream_t sg, cudaStream_t so, cudaEvent_t e_in,
                                cudaEvent_t e_gemm) {
   nw_status_t st;
+  if (fused_c1_eligible(p, g)) {  // one input channel: V and M never leave the SM
+    if ((st = launch_fused_c1(p, g, x, U, y, si)) != NW_OK) return st;
+    if (si != so) {
+      if (cudaEventRecord(e_in, si) != cudaSuccess || cudaStreamWaitEvent(so, e_in, 0) != cudaSuccess)
+        return NW_ERR_CUDA;
+    }
+    return NW_OK;
+  }
   if ((st = launch_input_transform(p, g, x, V, si)) != NW_OK) return st;
   if (si != sg) {
     if (cudaEventRecord(e_in, si) != cudaSuccess || cudaStreamWaitEvent(sg, e_in, 0) != cudaSuccess) return NW_ERR_CUDA;

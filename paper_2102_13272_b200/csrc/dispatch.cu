@@ -1,5 +1,7 @@
 // dispatch.cu -- route a geometry's axis kernel (m_o, r_o, m_i) to its compiled transform kernels
 // (the plan's nested kernel, or F(1,1) (x) F(3,3) = single-level F(3,3) for the OLA path).
+#include <cstdlib>
+
 #include "nw_internal.h"
 
 namespace nw {
@@ -10,6 +12,9 @@ template <int MO, int RO, int MI>
 nw_status_t output_impl(const nw_plan_st*, const Geometry&, const float*, void*, cudaStream_t);
 template <int MO, int RO, int MI>
 nw_status_t output_impl_pre(const nw_plan_st*, const Geometry&, const float*, void*, cudaStream_t);
+
+template <int MO, int RO, int MI>
+nw_status_t fused_c1_impl(const nw_plan_st*, const Geometry&, const void*, const void*, void*, cudaStream_t);
 
 #define NW_DISPATCH_AXIS(p, FN, ...)                                       \
   do {                                                                     \
@@ -37,6 +42,20 @@ nw_status_t launch_output_transform(const nw_plan_st* p, const Geometry& g, cons
 nw_status_t launch_output_transform_pre(const nw_plan_st* p, const Geometry& g, const float* M, void* y,
                                         cudaStream_t s) {
   NW_DISPATCH_AXIS(p, output_impl_pre, p, g, M, y, s);
+}
+
+bool fused_c1_eligible(const nw_plan_st* p, const Geometry& g) {
+  static const int on = [] {
+    const char* v = getenv("NW_FUSED_C1");
+    return v ? atoi(v) : 1;
+  }();
+  return on && g.path == kPathNested && g.mode == 0 && g.cin_e == 1 && g.mi == 3 && g.nph == 1 && g.mo >= 2 &&
+         g.Pa <= 30;  // V of 32 slices in shared memory: up to F(4,3) / F(5,2) (x) F(3,3)
+}
+
+nw_status_t launch_fused_c1(const nw_plan_st* p, const Geometry& g, const void* x, const void* U, void* y,
+                            cudaStream_t s) {
+  NW_DISPATCH_AXIS(p, fused_c1_impl, p, g, x, U, y, s);
 }
 
 }  // namespace nw

@@ -107,6 +107,10 @@ nw_status_t launch_output_transform_pre(const nw_plan_st *p, const Geometry &g, 
                                         cudaStream_t s);
 nw_status_t launch_gemm_tc(const nw_plan_st *p, const Geometry &g, const void *V, const void *U,
                            float *M, cudaStream_t s);
+// single-input-channel layers: the whole nested pipeline in one kernel (fused_small.cuh)
+bool fused_c1_eligible(const nw_plan_st *p, const Geometry &g);
+nw_status_t launch_fused_c1(const nw_plan_st *p, const Geometry &g, const void *x, const void *U, void *y,
+                            cudaStream_t s);
 
 // Launch with programmatic stream serialization (PDL): the kernel may start while the
 // previous kernel in the stream drains; it calls griddepcontrol.wait before reading

@@ -92,10 +92,12 @@ __device__ __forceinline__ float csel(const float (&v)[kMaxL], int i) {
   return r;
 }
 
-template <int MO, int RO, int MI, typename YT, bool PRE, int PART>
-__device__ __forceinline__ void out_consume(const float* ring, uint64_t* full, uint64_t* empty, float* ystage,
-                                            long long* sinfo, YT* __restrict__ y, const Geometry& g,
-                                            const float* __restrict__ slopes, int nunits, int ngroups) {
+// One unit = 32 slices (lanes) x one output channel coe, one column part: accumulates
+// Y = A^T_hat M A_hat from the point rows rowsrc(r, mv) delivers (r = p_o * l_i + p_i),
+// then stores the tile (keep mask, crop, depth-to-space, PReLU, cast).
+template <int MO, int RO, int MI, typename YT, bool PRE, int PART, typename RowSrc>
+__device__ __forceinline__ void out_unit(long long t0, int coe, RowSrc&& rowsrc, float* yst, long long* info,
+                                         YT* __restrict__ y, const Geometry& g, const float* __restrict__ slopes) {
   using X = Ax<MO, RO, MI>;
   using C = OutCfg<MO, RO, MI, PRE>;
   constexpr AxisF F = axis_f(MO, RO, MI);
@@ -104,18 +106,11 @@ __device__ __forceinline__ void out_consume(const float* ring, uint64_t* full, u
   constexpr int RL = C::RL;
   constexpr int QW = C::QW;
   constexpr int T0 = PART * C::TH;                              // first outer output of this part
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cw_ = warp / C::SPL;                                // channel within unit
-  float* yst = ystage + warp * C::YST;
-  long long* info = sinfo + warp * (C::TS * 2);
+  const int lane = threadIdx.x & 31;
   const long long HoWo = (long long)g.Ho * g.Wo;
   const int rowstride = (g.mode == 2) ? 2 * g.Wo : g.Wo;
   const int colstride = (g.mode == 2) ? 2 : 1;
-  int st = 0;
-  uint32_t ph = 0;
-  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-    const long long t0 = (long long)(u / ngroups) * C::TS;
-    const int coe = (u % ngroups) * C::CO + cw_;
+  {
 
     float Y[MA][QW];
 #pragma unroll
@@ -132,14 +127,8 @@ __device__ __forceinline__ void out_consume(const float* ring, uint64_t* full, u
         for (int j = 0; j < QW; ++j) uacc[s][j] = 0.f;
 #pragma unroll
       for (int p_i = 0; p_i < LI; ++p_i) {
-        ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
-        const float* src = ring + st * C::STAGE + cw_ * C::TS + lane;
         float mv[RL], qv[QW];
-#pragma unroll
-        for (int p_w = 0; p_w < RL; ++p_w) mv[p_w] = src[p_w * (C::CO * C::TS)];
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[st]));
-        if (++st == C::NST) { st = 0; ph ^= 1; }
+        rowsrc(p_o * LI + p_i, mv);
         // inner level along w on every outer point (done by the contraction epilogue when PRE)
         float uw[LO][MI];
 #pragma unroll
@@ -287,6 +276,35 @@ __device__ __forceinline__ void out_consume(const float* ring, uint64_t* full, u
       }
       __syncwarp();
     }
+  }
+}
+
+template <int MO, int RO, int MI, typename YT, bool PRE, int PART>
+__device__ __forceinline__ void out_consume(const float* ring, uint64_t* full, uint64_t* empty, float* ystage,
+                                            long long* sinfo, YT* __restrict__ y, const Geometry& g,
+                                            const float* __restrict__ slopes, int nunits, int ngroups) {
+  using C = OutCfg<MO, RO, MI, PRE>;
+  constexpr int RL = C::RL;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cw_ = warp / C::SPL;                                // channel within unit
+  float* yst = ystage + warp * C::YST;
+  long long* info = sinfo + warp * (C::TS * 2);
+  int st = 0;
+  uint32_t ph = 0;
+  // point rows stream through the TMA ring
+  auto ring_row = [&](int, float(&mv)[RL]) {
+    ptx::mbar_wait(ptx::smem_u32(&full[st]), ph);
+    const float* src = ring + st * C::STAGE + cw_ * C::TS + lane;
+#pragma unroll
+    for (int p_w = 0; p_w < RL; ++p_w) mv[p_w] = src[p_w * (C::CO * C::TS)];
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&empty[st]));
+    if (++st == C::NST) { st = 0; ph ^= 1; }
+  };
+  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const long long t0 = (long long)(u / ngroups) * C::TS;
+    const int coe = (u % ngroups) * C::CO + cw_;
+    out_unit<MO, RO, MI, YT, PRE, PART>(t0, coe, ring_row, yst, info, y, g, slopes);
   }
 }
 

@@ -2,9 +2,12 @@
 // (outer kernel over a 2-tile grid: filters of up to 6 taps per phase, R8).
 #include "input_transform.cuh"
 #include "output_transform.cuh"
+#include "fused_small.cuh"
 
 namespace nw {
 template nw_status_t input_impl<4, 2, 3>(const nw_plan_st*, const Geometry&, const void*, void*, cudaStream_t);
 template nw_status_t output_impl<4, 2, 3>(const nw_plan_st*, const Geometry&, const float*, void*, cudaStream_t);
 template nw_status_t output_impl_pre<4, 2, 3>(const nw_plan_st*, const Geometry&, const float*, void*, cudaStream_t);
+template nw_status_t fused_c1_impl<4, 2, 3>(const nw_plan_st*, const Geometry&, const void*, const void*, void*,
+                                                  cudaStream_t);
 }  // namespace nw
