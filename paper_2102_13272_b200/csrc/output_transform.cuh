@@ -246,6 +246,9 @@ __device__ __forceinline__ void out_unit(long long t0, int coe, RowSrc&& rowsrc,
         for (int j = 0; j < QW; ++j)
           if (hph * HR + i < MA) yst[lane * (HR * QW) + i * QW + j] = Y[(hph * HR + i < MA) ? hph * HR + i : 0][j];
       __syncwarp();
+      // m_i = 3 (no coverage phases): output positions are the identity and every tile
+      // output is kept, so only the crop limits are tested per element
+      constexpr bool kSimple = (MI == kRi);
 #pragma unroll 1
       for (int jj = 0; jj < QW; ++jj) {
         const int e = lane + 32 * jj;  // (slice s, local column ql) pairs, ql fastest
@@ -256,21 +259,29 @@ __device__ __forceinline__ void out_unit(long long t0, int coe, RowSrc&& rowsrc,
         const int lim = (int)ptx::lds_s64(ia + 8);
         const uint32_t ya = ptx::smem_u32(yst) + (uint32_t)(s * (HR * QW) + ql) * 4u;
         const int limh = lim & 255, limw = (lim >> 8) & 255;
-        const int khi = (lim >> 16) & 3, kwi = (lim >> 18) & 3;
-        const unsigned kh = khi == 0 ? OT.keep[0] : khi == 1 ? OT.keep[1] : OT.keep[2];
-        const unsigned kw = kwi == 0 ? OT.keep[0] : kwi == 1 ? OT.keep[1] : OT.keep[2];
-        int pw = 0;
+        unsigned kh = ~0u;
+        int pw = q_w;
+        bool okw;
+        if constexpr (kSimple) {
+          okw = b >= 0 && (qw0 + QW <= MA || q_w < MA) && q_w < limw;
+        } else {
+          const int khi = (lim >> 16) & 3, kwi = (lim >> 18) & 3;
+          kh = khi == 0 ? OT.keep[0] : khi == 1 ? OT.keep[1] : OT.keep[2];
+          const unsigned kw = kwi == 0 ? OT.keep[0] : kwi == 1 ? OT.keep[1] : OT.keep[2];
+          pw = 0;
 #pragma unroll
-        for (int q = 0; q < MA; ++q) pw = (q_w == q) ? OT.pos[q] : pw;
-        const bool okw = b >= 0 && q_w < MA && ((kw >> q_w) & 1u) && pw < limw;
-        YT* dst = y + (b < 0 ? 0 : b) + (long long)pw * colstride;
+          for (int q = 0; q < MA; ++q) pw = (q_w == q) ? OT.pos[q] : pw;
+          okw = b >= 0 && q_w < MA && ((kw >> q_w) & 1u) && pw < limw;
+        }
+        YT* dst = y + (b < 0 ? 0 : b) + pw * colstride;
 #pragma unroll
         for (int i = 0; i < HR; ++i) {
           const int q_h = hph * HR + i;
-          if (q_h < MA && okw && ((kh >> q_h) & 1u) && OT.pos[q_h < MA ? q_h : 0] < limh) {
+          const bool kept = kSimple || ((kh >> q_h) & 1u);
+          if (q_h < MA && okw && kept && OT.pos[q_h < MA ? q_h : 0] < limh) {
             float v = ptx::lds_f32(ya + i * QW * 4);
             if (slopes) v = v >= 0.f ? v : slope * v;
-            dst[(long long)OT.pos[q_h < MA ? q_h : 0] * rowstride] = from_f<YT>(v);
+            dst[OT.pos[q_h < MA ? q_h : 0] * rowstride] = from_f<YT>(v);  // 32-bit row offset
           }
         }
       }
