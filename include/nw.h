@@ -113,6 +113,9 @@ typedef struct {
   size_t filter_bytes; /* bytes of U for nw_transform_filter */
   int m_rows;          /* transform-domain rows per slice the contraction writes: points, or
                           P_a * l_o * m_i when the inner output level is fused into its epilogue */
+  int single_kernel;   /* 1: nw_conv_forward runs the layer as ONE kernel (one input channel: the
+                          contraction is a pointwise product, V and M stay on chip; no workspace
+                          traffic), 0: input transform, contraction, output transform */
 } nw_plan_info_t;
 
 /* Create a plan for a K x K convolution with the given stride (1 or 2) using

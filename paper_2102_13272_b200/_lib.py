@@ -36,7 +36,8 @@ class PlanInfo(ctypes.Structure):
         "K", "stride", "transposed", "pad", "output_padding", "m_outer", "r_outer", "m_inner",
         "points_axis", "points", "window", "tile_out", "n_phase", "Kp", "cin", "cout", "cin_e",
         "cout_e", "cin_pad", "cout_pad", "math", "dtype")] + [("filter_bytes", ctypes.c_size_t),
-                                                              ("m_rows", ctypes.c_int)]
+                                                              ("m_rows", ctypes.c_int),
+                                                              ("single_kernel", ctypes.c_int)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -30,6 +30,7 @@ class NestedConv2d:
         Cin, Cout = (w.shape[0], w.shape[1]) if transposed else (w.shape[1], w.shape[0])
         self.w = w.contiguous()
         self.dtype = w.dtype
+        self.prelu_slopes = prelu_slopes
         self.plan = Plan(K, stride, m_outer, m_inner, Cin, Cout, math=math, dtype=_DT[w.dtype],
                          transposed=transposed, output_padding=output_padding, outer_taps=outer_taps,
                          pad=pad, prelu_slopes=prelu_slopes)

@@ -295,6 +295,8 @@ nw_status_t nw_plan_info(nw_plan_t p, nw_plan_info_t *info) {
   {
     Geometry g = make_geometry(p, 1, 3 * p->K + 16, 3 * p->K + 16);
     info->m_rows = gemm_fused_eligible(p, g) ? p->ax.Pa * p->ax.l_o * p->m_i : info->points;
+    info->single_kernel = fused_c1_eligible(p, g) ? 1 : 0;
+    if (info->single_kernel) info->m_rows = 0;
   }
   return NW_OK;
 }

@@ -126,6 +126,18 @@ def test_m_rows_reports_fused_inner_output_level():
     assert _lib.Plan(9, 1, 4, 3, 64, 64, math=_lib.MATH_FP32_SIMT).info()["m_rows"] == 900
 
 
+def test_single_kernel_for_one_input_channel():
+    # Cin = 1 (stride 1, m_i = 3): the contraction over input channels (Eq. 2.1) is one product per
+    # point, so the layer runs as one on-chip kernel and writes no transform-domain rows
+    for K, m_o, r_o in ((5, 4, 0), (9, 4, 3), (7, 3, 3)):
+        inf = _lib.Plan(K, 1, m_o, 3, 1, 32, outer_taps=r_o).info()
+        assert inf["single_kernel"] == 1 and inf["m_rows"] == 0
+    assert _lib.Plan(9, 1, 5, 3, 1, 32).info()["single_kernel"] == 0      # V of 32 slices exceeds smem
+    assert _lib.Plan(5, 2, 4, 3, 1, 32).info()["single_kernel"] == 0      # stride 2: 4 phase channels
+    assert _lib.Plan(5, 1, 2, 2, 1, 32).info()["single_kernel"] == 0      # coverage phases (m_i = 2)
+    assert _lib.Plan(5, 1, 4, 3, 2, 32).info()["single_kernel"] == 0
+
+
 def test_forward_argument_errors_without_touching_memory():
     # argument validation happens before any CUDA call: fake (never dereferenced) pointers suffice
     lib = _lib.load()

@@ -19,8 +19,8 @@ TOL = {"fp32": 1e-4, "bf16x3": 5e-3}
 
 
 def _math(name):
-    from paper_2102_13272_b200 import MATH_BF16X3, MATH_FP32_SIMT
-    return {"fp32": MATH_FP32_SIMT, "bf16x3": MATH_BF16X3}[name]
+    from paper_2102_13272_b200 import MATH_BF16, MATH_BF16X3, MATH_FP32_SIMT
+    return {"fp32": MATH_FP32_SIMT, "bf16x3": MATH_BF16X3, "bf16": MATH_BF16}[name]
 
 
 def _run(layer, math, prelu=False):

@@ -46,7 +46,7 @@ KEYS = [
 STALLS = re.compile(r"^smsp__average_warps_issue_stalled_(\w+)_per_issue_active\.ratio$")
 KIND = {"input_transform": "input_transform", "contraction": "contraction_tc",
         "output_transform": "output_transform", "gemm_simt": "contraction_fp32_simt",
-        "filter_transform": "filter_transform", "ola": "ola", "direct": "direct"}
+        "filter_transform": "filter_transform", "ola": "ola", "direct": "direct", "fused_c1": "fused_c1"}
 
 
 def short(name: str) -> str:
