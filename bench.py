@@ -381,7 +381,7 @@ def main():
     if not args.no_compare and args.path == "nested" and not chain:
         # ola / direct: same kernels and math mode as the nested line.  direct_bf16: the direct
         # path in its cheapest mode that meets the same 5e-3 gate (plain bf16
-        # passes for direct, not for OLA or nested -- tests/test_gpu_math_modes.py, R22)
+        # passes for direct, not for OLA or nested -- tests/test_gpu_math_modes.py, R21)
         legs = [("ola", "ola", None), ("direct", "direct", None)]
         if args.math == "bf16x3":
             legs.append(("direct_bf16", "direct", nw.MATH_BF16))
@@ -456,13 +456,21 @@ def main():
         for conv, x in zip(convs, xs):
             nbytes = conv.plan.workspace_size(x.shape[0], x.shape[2], x.shape[3], "host")
             wss.append(nbytes)
-        ws_host = torch.empty(max(wss), dtype=torch.uint8, device=dev)
+        # the sweep's layers are independent: each runs on its own stream with its own workspace,
+        # so one layer's copies in overlap another's copies out (PCIe carries both directions)
+        ws_l = [torch.empty(n, dtype=torch.uint8, device=dev) for n in wss]
+        # host chunks per call: 4 measured best with the layers overlapping (C2: 1 / 2 / 4 / 8 / 16
+        # chunks -> 54 / 72 / 73 / 70 / 64 TFLOP/s, profiles/r3_e2e_chunks.md); read per call
+        os.environ.setdefault("NW_HOST_CHUNKS", "4")
+        streams = [torch.cuda.Stream(device=dev) for _ in convs]
 
         def e2e_step():
-            for conv, x, hxx, hyy in zip(convs, xs, hx, hy):
-                conv.plan.forward_host(hxx, conv.U, hyy, x.shape[0], x.shape[2], x.shape[3], ws_host,
-                                       ws_host.numel())
+            for conv, x, hxx, hyy, wsx, st in zip(convs, xs, hx, hy, ws_l, streams):
+                conv.plan.forward_host(hxx, conv.U, hyy, x.shape[0], x.shape[2], x.shape[3], wsx, wsx.numel(),
+                                       stream=st)
 
+        for st in streams:
+            st.wait_stream(stream)
         for _ in range(2):
             e2e_step()
         torch.cuda.synchronize()
@@ -471,8 +479,12 @@ def main():
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ek = max(3, args.steps // 4)
         s0.record(stream)
+        for st in streams:
+            st.wait_stream(stream)
         for _ in range(ek):
             e2e_step()
+        for st in streams:
+            stream.wait_stream(st)
         s1.record(stream)
         torch.cuda.synchronize()
         ems = nwd.max_over_ranks(s0.elapsed_time(s1) / ek, dev)
