@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
   if constexpr (sizeof(XT) == 4) {
   constexpr int NT1 = (CC * C::WSC + C::THREADS - 1) / C::THREADS;
   float xr[NT1][C::PROWS];
+  const bool rin = row0 + p >= 0 && row0 + p + SR * (C::PROWS - 1) < g.H;
 #pragma unroll
   for (int i = 0; i < NT1; ++i) {
     const int task = tid + i * C::THREADS;
@@ -149,13 +150,23 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
     const bool cok = task < CC * C::WSC && ci < g.Cin && gc >= 0 && gc < g.W;
     const XT* rp = x + (((long long)n * g.Cin + (cok ? ci : 0)) * g.H) * g.W + (cok ? gc : 0) +
                    (long long)(row0 + p) * g.W;
+    if (rin) {  // block-uniform: the whole window column inside the image, no row tests
 #pragma unroll
-    for (int r = 0; r < C::PROWS; ++r) {
-      const int gr = row0 + p + SR * r;
-      xr[i][r] = (cok && gr >= 0 && gr < g.H) ? to_f(*rp) : 0.f;
-      long long w = (long long)SR * g.W;
-      asm volatile("" : "+l"(w));
-      rp += w;
+      for (int r = 0; r < C::PROWS; ++r) {
+        xr[i][r] = cok ? to_f(*rp) : 0.f;
+        long long w = (long long)SR * g.W;
+        asm volatile("" : "+l"(w));
+        rp += w;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < C::PROWS; ++r) {
+        const int gr = row0 + p + SR * r;
+        xr[i][r] = (cok && gr >= 0 && gr < g.H) ? to_f(*rp) : 0.f;
+        long long w = (long long)SR * g.W;
+        asm volatile("" : "+l"(w));
+        rp += w;
+      }
     }
   }
 #pragma unroll
@@ -302,16 +313,17 @@ static nw_status_t input_pick(const Geometry& g, const void* x, void* V, cudaStr
     const char* v = getenv("NW_IN_CC");
     return v ? atoi(v) : 32;
   }();
-  if (SR == 2) {  // 4 contraction channels per source channel; narrow layers (C4a: 3) take 8-channel CTAs
+  if constexpr (SR == 2) {  // 4 contraction channels per source channel; narrow layers (C4a: 3) take 8-channel CTAs
     if (g.cs <= 8) return input_launch<MO, RO, MI, SR, 8, XT, BF>(g, x, V, s);
     return input_launch<MO, RO, MI, SR, 16, XT, BF>(g, x, V, s);
+  } else {
+    if constexpr (Ax<MO, RO, MI>::NPH == 1) {
+      if (cc >= 64 && g.cin_pad >= 64 && InCfg<MO, RO, MI, SR, 64>::SMEM <= 227 * 1024)
+        return input_launch<MO, RO, MI, SR, 64, XT, BF>(g, x, V, s);
+      if (cc >= 32 && g.cin_pad >= 32) return input_launch<MO, RO, MI, SR, 32, XT, BF>(g, x, V, s);
+    }
+    return input_launch<MO, RO, MI, SR, 16, XT, BF>(g, x, V, s);
   }
-  if (Ax<MO, RO, MI>::NPH == 1) {
-    if (cc >= 64 && g.cin_pad >= 64 && InCfg<MO, RO, MI, SR, 64>::SMEM <= 227 * 1024)
-      return input_launch<MO, RO, MI, SR, 64, XT, BF>(g, x, V, s);
-    if (cc >= 32 && g.cin_pad >= 32) return input_launch<MO, RO, MI, SR, 32, XT, BF>(g, x, V, s);
-  }
-  return input_launch<MO, RO, MI, SR, 16, XT, BF>(g, x, V, s);
 }
 
 // Instantiated per axis combo in xform_<mo><ro><mi>.cu.  Stride-2 phases and
