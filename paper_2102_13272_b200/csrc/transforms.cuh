@@ -118,6 +118,67 @@ struct K1<4, 3> {
   }
 };
 
+// Factored kernels are checked at compile time against the exact Cook-Toom tables (plan.cu's
+// source of truth): the table a specialization hard-codes must equal make_kernel's.
+__host__ __device__ constexpr bool bt_equal(int m1, int r1, int m2, int r2) {
+  const Kernel1D a = make_kernel(m1, r1), b = make_kernel(m2, r2);
+  if (a.l != b.l) return false;
+  for (int i = 0; i < a.l; ++i)
+    for (int j = 0; j < a.l; ++j)
+      if (rdouble(a.BT[i][j]) != rdouble(b.BT[i][j])) return false;
+  return true;
+}
+template <int M, int L>
+__host__ __device__ constexpr bool at_equals(int r, const int (&t)[M][L]) {
+  const Kernel1D k = make_kernel(M, r);
+  if (k.l != L) return false;
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < L; ++j)
+      if (rdouble(k.AT[i][j]) != double(t[i][j])) return false;
+  return true;
+}
+
+// F(4,2): points {0, 1, -1, 2, inf}, the point set of F(3,3), so B^T is F(3,3)'s
+//   A^T = [1 1 1 1 0; 0 1 -1 2 0; 0 1 1 4 0; 0 1 -1 8 1]
+constexpr int kAT42[4][5] = {{1, 1, 1, 1, 0}, {0, 1, -1, 2, 0}, {0, 1, 1, 4, 0}, {0, 1, -1, 8, 1}};
+static_assert(bt_equal(4, 2, 3, 3) && at_equals<4, 5>(2, kAT42), "F(4,2) tables");
+template <>
+struct K1<4, 2> {
+  static constexpr int L = 5;
+  __device__ __forceinline__ static void bt(const float (&x)[5], float (&o)[5]) { K1<3, 3>::bt(x, o); }
+  __device__ __forceinline__ static void at(const float (&x)[5], float (&o)[4]) {
+    const float s = x[1] + x[2], d = x[1] - x[2];
+    o[0] = (x[0] + x[3]) + s;                            // x0 + x1 + x2 + x3
+    o[1] = fmaf(2.f, x[3], d);                           // x1 - x2 + 2x3
+    o[2] = fmaf(4.f, x[3], s);                           // x1 + x2 + 4x3
+    o[3] = fmaf(8.f, x[3], d) + x[4];                    // x1 - x2 + 8x3 + x4
+  }
+};
+
+// F(5,2): points {0, 1, -1, 2, -2, inf}, the point set of F(4,3), so B^T is F(4,3)'s
+//   A^T = [1 1 1 1 1 0; 0 1 -1 2 -2 0; 0 1 1 4 4 0; 0 1 -1 8 -8 0; 0 1 1 16 16 1]
+constexpr int kAT52[5][6] = {{1, 1, 1, 1, 1, 0}, {0, 1, -1, 2, -2, 0}, {0, 1, 1, 4, 4, 0}, {0, 1, -1, 8, -8, 0},
+                             {0, 1, 1, 16, 16, 1}};
+static_assert(bt_equal(5, 2, 4, 3) && at_equals<5, 6>(2, kAT52), "F(5,2) tables");
+template <>
+struct K1<5, 2> {
+  static constexpr int L = 6;
+  __device__ __forceinline__ static void bt(const float (&x)[6], float (&o)[6]) { K1<4, 3>::bt(x, o); }
+  __device__ __forceinline__ static void at(const float (&x)[6], float (&o)[5]) {
+    const float s1 = x[1] + x[2], d1 = x[1] - x[2], s2 = x[3] + x[4], d2 = x[3] - x[4];
+    o[0] = (x[0] + s1) + s2;                             // x0 + x1 + x2 + x3 + x4
+    o[1] = fmaf(2.f, d2, d1);                            // x1 - x2 + 2x3 - 2x4
+    o[2] = fmaf(4.f, s2, s1);                            // x1 + x2 + 4x3 + 4x4
+    o[3] = fmaf(8.f, d2, d1);                            // x1 - x2 + 8x3 - 8x4
+    o[4] = fmaf(16.f, s2, s1) + x[5];                    // x1 + x2 + 16x3 + 16x4 + x5
+  }
+};
+
+// the hand-written F(3,3) / F(4,3) tables above, checked the same way
+constexpr int kAT33[3][5] = {{1, 1, 1, 1, 0}, {0, 1, -1, 2, 0}, {0, 1, 1, 4, 1}};
+constexpr int kAT43[4][6] = {{1, 1, 1, 1, 1, 0}, {0, 1, -1, 2, -2, 0}, {0, 1, 1, 4, 4, 0}, {0, 1, -1, 8, -8, 1}};
+static_assert(at_equals<3, 5>(3, kAT33) && at_equals<4, 6>(3, kAT43), "F(3,3) / F(4,3) output tables");
+
 // ---------------------------------------------------------------------------
 // per-axis two-level transforms, float
 // ---------------------------------------------------------------------------
