@@ -15,6 +15,7 @@
 // inside each call (into the workspace).
 #include <cuda_bf16.h>
 
+#include "ptx.cuh"
 #include "transforms.cuh"
 
 namespace nw {
@@ -62,10 +63,10 @@ __global__ void __launch_bounds__(256) pack_input_kernel(const XT* __restrict__ 
     const long long o = t * g.cin_pad + 2 * cp;
     if (BF) {
       __nv_bfloat16* V = reinterpret_cast<__nv_bfloat16*>(Vout);
-      const __nv_bfloat162 hi = __floats2bfloat162_rn(a, bb);
-      const float2 hf = __bfloat1622float2(hi);
-      *reinterpret_cast<__nv_bfloat162*>(V + o) = hi;
-      *reinterpret_cast<__nv_bfloat162*>(V + plane + o) = __floats2bfloat162_rn(a - hf.x, bb - hf.y);
+      uint32_t hi, lo;
+      ptx::split_bf16x2(a, bb, hi, lo);
+      *reinterpret_cast<uint32_t*>(V + o) = hi;
+      *reinterpret_cast<uint32_t*>(V + plane + o) = lo;
     } else {
       *reinterpret_cast<float2*>(reinterpret_cast<float*>(Vout) + o) = make_float2(a, bb);
     }

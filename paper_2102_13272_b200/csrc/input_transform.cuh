@@ -59,10 +59,10 @@ __device__ __forceinline__ void store_row(const float (*za)[Ax<MO, RO, MI>::LI],
 #pragma unroll
     for (int po = 0; po < X::LO; ++po) {
       if constexpr (BF) {
-        const __nv_bfloat162 hi = __floats2bfloat162_rn(oa[po], ob[po]);
-        const float2 hf = __bfloat1622float2(hi);
-        *reinterpret_cast<__nv_bfloat162*>(h) = hi;
-        *reinterpret_cast<__nv_bfloat162*>(l) = __floats2bfloat162_rn(oa[po] - hf.x, ob[po] - hf.y);
+        uint32_t hi, lo;
+        ptx::split_bf16x2(oa[po], ob[po], hi, lo);
+        *reinterpret_cast<uint32_t*>(h) = hi;
+        *reinterpret_cast<uint32_t*>(l) = lo;
       } else {
         *reinterpret_cast<float2*>(h) = make_float2(oa[po], ob[po]);
       }
@@ -93,11 +93,11 @@ __device__ __forceinline__ void store_row_imm(const float (*za)[Ax<MO, RO, MI>::
     in_axis_outer_col<MO, RO, MI>(zb, pi, ob);
 #pragma unroll
     for (int po = 0; po < X::LO; ++po) {
-      const __nv_bfloat162 hi = __floats2bfloat162_rn(oa[po], ob[po]);
-      const float2 hf = __bfloat1622float2(hi);
+      uint32_t hi, lo;
+      ptx::split_bf16x2(oa[po], ob[po], hi, lo);
       char* h = hp + (po * X::LI + pi) * PS;
-      *reinterpret_cast<__nv_bfloat162*>(h) = hi;
-      *reinterpret_cast<__nv_bfloat162*>(h + PL) = __floats2bfloat162_rn(oa[po] - hf.x, ob[po] - hf.y);
+      *reinterpret_cast<uint32_t*>(h) = hi;
+      *reinterpret_cast<uint32_t*>(h + PL) = lo;
     }
   }
 }

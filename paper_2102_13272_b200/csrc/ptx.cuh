@@ -9,6 +9,15 @@
 namespace nw {
 namespace ptx {
 
+// bf16x3 split of a value pair (R12): hi = bf16_rne(v), lo = bf16_rne(v - hi), packed
+// as bf16x2 {a in the low half, b in the high half}.  One cvt per plane; the hi halves are
+// widened back with a shift / mask (no permute, no conversion call).
+__device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(b), "f"(a));
+  const float ha = __uint_as_float(hi << 16), hb = __uint_as_float(hi & 0xffff0000u);
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(b - hb), "f"(a - ha));
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
