@@ -123,6 +123,7 @@ struct Params {
   int G;            // blocks per unit
   int ngrp;         // unit groups per point = ceil(nmb / G)
   int N;            // cout_pad (MMA N, <= 256)
+  int Nst;          // channels stored (cout_e): rows of padded channels are never read, not written
   int KB;           // k-blocks of 64 (ceil(cin_pad / 64))
   int lo;           // 1 = bf16x3 (lo planes), 0 = plain bf16
   int nA, nB;       // ring depths
@@ -308,13 +309,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int g = 0; g < g_eff; ++g) {
         const long long t = (long long)(mb0 + g) * kBM + row;
         float* dst = p.M + (long long)xi * p.N * p.T_pad + t;
-        for (int c0 = 0; c0 < p.N; c0 += 16) {
+        for (int c0 = 0; c0 < p.Nst; c0 += 16) {
           uint32_t r[16];
           const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * 256 + g * p.N + c0);
           tmem_ld16(taddr, r);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) dst[(long long)(c0 + j) * p.T_pad] = __uint_as_float(r[j]);
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j < p.Nst) dst[(long long)(c0 + j) * p.T_pad] = __uint_as_float(r[j]);
         }
       }
       fence_before();
@@ -541,6 +543,7 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   prm.P = g.P;
   prm.nmb = (int)(g.T_pad / tc::kBM);
   prm.N = g.cout_pad;
+  prm.Nst = g.cout_e;
   prm.G = 256 / prm.N;
   if (prm.G > 4) prm.G = 4;
   if (prm.G < 1) prm.G = 1;
