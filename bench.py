@@ -277,6 +277,10 @@ def cores_used():
 # ----------------------------------------------------------------------------
 def main():
     args = parse()
+    # host chunks per nw_conv_forward_host call (read once by the library, before any call): 4
+    # measured best with the e2e leg's layers overlapping (C2: 1 / 2 / 4 / 8 / 16 chunks ->
+    # 54 / 72 / 73 / 70 / 64 TFLOP/s, profiles/r3_e2e_chunks.md)
+    os.environ.setdefault("NW_HOST_CHUNKS", "4")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -459,9 +463,6 @@ def main():
         # the sweep's layers are independent: each runs on its own stream with its own workspace,
         # so one layer's copies in overlap another's copies out (PCIe carries both directions)
         ws_l = [torch.empty(n, dtype=torch.uint8, device=dev) for n in wss]
-        # host chunks per call: 4 measured best with the layers overlapping (C2: 1 / 2 / 4 / 8 / 16
-        # chunks -> 54 / 72 / 73 / 70 / 64 TFLOP/s, profiles/r3_e2e_chunks.md); read per call
-        os.environ.setdefault("NW_HOST_CHUNKS", "4")
         streams = [torch.cuda.Stream(device=dev) for _ in convs]
 
         def e2e_step():

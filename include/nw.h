@@ -34,8 +34,10 @@
  *    channels per input-transform CTA (default 32); NW_PIPE_CHUNKS=k runs
  *    nw_conv_forward as a k-chunk three-stream pipeline (default 1) and
  *    NW_GEMM_CTAS caps its contraction grid; NW_HOST_CHUNKS=k sets the chunk
- *    count of nw_conv_forward_host (default 8); NW_PDL=1 launches the three hot
- *    kernels with programmatic dependent launch.
+ *    count of nw_conv_forward_host (default 8; read once, at the first host-path
+ *    call or workspace query, so sizes stay consistent); NW_PDL=1 launches the
+ *    three hot kernels with programmatic dependent launch; NW_FUSED_C1=0 turns
+ *    off the single-kernel path for one-input-channel layers.
  */
 #ifndef NW_H_
 #define NW_H_

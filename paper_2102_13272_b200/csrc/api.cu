@@ -162,7 +162,7 @@ extern "C" {
 static int host_chunk(int N) {
   // images per full chunk: ~NW_HOST_CHUNKS chunks (default 8); the schedule ramps up and
   // down around it so the pipeline fill (first H2D) and drain (last D2H) stay short
-  const int k = env_int("NW_HOST_CHUNKS", 8);
+  static const int k = env_int("NW_HOST_CHUNKS", 8);  // once per process: workspace sizes stay consistent
   int nc = (N + (k > 0 ? k : 1) - 1) / (k > 0 ? k : 1);
   return nc < 1 ? 1 : nc;
 }

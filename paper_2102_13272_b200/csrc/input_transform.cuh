@@ -138,7 +138,10 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
   // fp32 x: every load of the thread's NT1 columns is issued before the first transform,
   // so a CTA waits for one global round trip per row phase instead of one per column
   // (measured faster for C2; bf16 x (C3) keeps the column-at-a-time loop, which measured faster)
-  if constexpr (sizeof(XT) == 4) {
+#ifndef NW_IN_BATCH_BF16
+#define NW_IN_BATCH_BF16 1
+#endif
+  if constexpr (sizeof(XT) == 4 || NW_IN_BATCH_BF16) {
   constexpr int NT1 = (CC * C::WSC + C::THREADS - 1) / C::THREADS;
   float xr[NT1][C::PROWS];
   const bool rin = row0 + p >= 0 && row0 + p + SR * (C::PROWS - 1) < g.H;
@@ -195,10 +198,11 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
       const XT* rp = x + (((long long)n * g.Cin + (cok ? ci : 0)) * g.H) * g.W + (cok ? gc : 0) +
                      (long long)(row0 + p) * g.W;
       float xc[C::PROWS];
+      const bool rin = row0 + p >= 0 && row0 + p + SR * (C::PROWS - 1) < g.H;
 #pragma unroll
       for (int r = 0; r < C::PROWS; ++r) {
         const int gr = row0 + p + SR * r;
-        xc[r] = (cok && gr >= 0 && gr < g.H) ? to_f(*rp) : 0.f;
+        xc[r] = (cok && (rin || (gr >= 0 && gr < g.H))) ? to_f(*rp) : 0.f;
         long long w = (long long)SR * g.W;
         asm volatile("" : "+l"(w));
         rp += w;

@@ -161,3 +161,12 @@ def test_wide_output_cta_pairs(Cout, N, H, W):
     layer = synth.small(synth.CONFIGS["c3"], N=N, H=H, W=W, Cin=64, Cout=Cout)
     t, y = _run(layer, "bf16x3")
     assert rel_err(y, _ref(layer, t)) <= max(TOL["bf16x3"], 2.0 ** -8)
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16x3"])
+def test_stride2_full_channel_pitch(math):
+    # stride 2 with 64 source channels: 4 x 64 = 256 phase-major contraction channels, the
+    # compile-time channel pitch of the V stores (C4b's layout) -- every output checked
+    layer = synth.small(synth.CONFIGS["c4b"], N=1, H=40, W=37, Cin=64, Cout=32)
+    t, y = _run(layer, math)
+    assert rel_err(y, _ref(layer, t)) <= TOL[math]

@@ -9,7 +9,7 @@ kill $SMI
 timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-compare > gpurun_out/plain_$TAG.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-compare > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "launches rc=$?"
-for LAYER in c2k5 c2k7 c2k9 c3; do
+for LAYER in c2k5 c2k7 c2k9 c3 c5_conv1; do
   timeout 300 python tools/prof_layer.py $LAYER --iters 2 > gpurun_out/prof_plain_${TAG}_$LAYER.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/dram_${TAG}_$LAYER.csv python tools/prof_layer.py $LAYER --iters 2 > /dev/null 2>&1; echo "dram $LAYER rc=$?"
@@ -19,4 +19,6 @@ for K in input_transform contraction output_transform; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 \
     -o gpurun_out/prof_${TAG}_${LAYER}_$K python tools/prof_layer.py $LAYER > gpurun_out/ncu_${K}_${TAG}_$LAYER.log 2>&1; echo "ncu $LAYER $K rc=$?"
 done; done
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_c1 -s 1 -c 1 \
+  -o gpurun_out/prof_${TAG}_c5conv1_fused_c1 python tools/prof_layer.py c5_conv1 > gpurun_out/ncu_fused_${TAG}.log 2>&1; echo "ncu c5_conv1 fused_c1 rc=$?"
 du -sh gpurun_out
