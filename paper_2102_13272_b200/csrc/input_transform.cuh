@@ -305,6 +305,8 @@ static nw_status_t input_launch(const Geometry& g, const void* x, void* V, cudaS
   if constexpr (BF && SR == 1) {
     if (g.vblk && g.cin_pad == 64) return input_launch_c<MO, RO, MI, SR, CC, XT, BF, 64>(g, x, V, s);
     if (g.vblk && g.cin_pad == 256) return input_launch_c<MO, RO, MI, SR, CC, XT, BF, 256>(g, x, V, s);
+    if constexpr (CC == 32)  // C5 deconv (32 source channels)
+      if (g.vblk && g.cin_pad == 32) return input_launch_c<MO, RO, MI, SR, CC, XT, BF, 32>(g, x, V, s);
   }
   if constexpr (BF && SR == 2 && sizeof(XT) == 4) {  // C4a (4 x 3 phase channels -> 16), C4b (4 x 64)
     if (g.vblk && g.cin_pad == 16 && CC == 8) return input_launch_c<MO, RO, MI, SR, CC, XT, BF, 16>(g, x, V, s);
