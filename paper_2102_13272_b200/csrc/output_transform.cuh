@@ -399,7 +399,7 @@ static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const f
   const uint32_t box[3] = {(uint32_t)C::TS, (uint32_t)C::CO, (uint32_t)C::RL};
   if (!encode_tmap(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, M, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
     return NW_ERR_CUDA;
-  const int ngroups = (g.cout_pad + C::CO - 1) / C::CO;
+  const int ngroups = (g.cout_e + C::CO - 1) / C::CO;  // channel groups holding real channels only
   const long long tchunks = (g.T + C::TS - 1) / C::TS;
   const long long nunits = tchunks * ngroups;
   int sms = 148, dev = 0;

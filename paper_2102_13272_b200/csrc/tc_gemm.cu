@@ -309,14 +309,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int g = 0; g < g_eff; ++g) {
         const long long t = (long long)(mb0 + g) * kBM + row;
         float* dst = p.M + (long long)xi * p.N * p.T_pad + t;
+        const long long ts = p.T_pad;
         for (int c0 = 0; c0 < p.Nst; c0 += 16) {
           uint32_t r[16];
           const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * 256 + g * p.N + c0);
           tmem_ld16(taddr, r);
           tmem_ld_wait();
+          float* d = dst + (long long)c0 * ts;
+          const int nj = p.Nst - c0;
+          if (nj >= 16) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < p.Nst) dst[(long long)(c0 + j) * p.T_pad] = __uint_as_float(r[j]);
+            for (int j = 0; j < 16; ++j) d[j * ts] = __uint_as_float(r[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nj) d[j * ts] = __uint_as_float(r[j]);
+          }
         }
       }
       fence_before();
@@ -544,8 +552,14 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   prm.nmb = (int)(g.T_pad / tc::kBM);
   prm.N = g.cout_pad;
   prm.Nst = g.cout_e;
+  // blocks per unit: fill the 256-column TMEM buffer (narrow N: up to 16 blocks share one B load
+  // and one round of unit synchronisation); NW_GEMM_G caps it
+  static const int g_cap = [] {
+    const char* v = getenv("NW_GEMM_G");
+    return v ? atoi(v) : 16;
+  }();
   prm.G = 256 / prm.N;
-  if (prm.G > 4) prm.G = 4;
+  if (prm.G > g_cap) prm.G = g_cap;
   if (prm.G < 1) prm.G = 1;
   prm.ngrp = (prm.nmb + prm.G - 1) / prm.G;
   if (g.nsh < 1 || g.nsh > kMaxShift) return NW_ERR_UNSUPPORTED;
@@ -567,7 +581,7 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   const uint32_t budget = 200 * 1024;
   prm.nB = 2;
   prm.nA = (int)((budget - prm.nB * b_stage) / a_stage);
-  if (prm.nA > 6) prm.nA = 6;
+  if (prm.nA > tc::kMaxStages) prm.nA = tc::kMaxStages;
   if (prm.nA < 2) {
     prm.nB = 1;
     prm.nA = (int)((budget - b_stage) / a_stage);
