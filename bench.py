@@ -277,10 +277,6 @@ def cores_used():
 # ----------------------------------------------------------------------------
 def main():
     args = parse()
-    # host chunks per nw_conv_forward_host call (read once by the library, before any call): 4
-    # measured best with the e2e leg's layers overlapping (C2: 1 / 2 / 4 / 8 / 16 chunks ->
-    # 54 / 72 / 73 / 70 / 64 TFLOP/s, profiles/r3_e2e_chunks.md)
-    os.environ.setdefault("NW_HOST_CHUNKS", "4")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -290,6 +286,12 @@ def main():
 
     if args.impl == "reference":
         return reference_arm(args, layers_all, world, rank)
+    if len(layers_all) > 1 and args.workload not in CHAINS:
+        # host chunks per nw_conv_forward_host call (read once by the library, before any call):
+        # with the e2e leg's independent layers overlapping on their own streams, 4 measured best
+        # (C2: 1 / 2 / 4 / 8 / 16 chunks -> 54 / 72 / 73 / 70 / 64 TFLOP/s,
+        # profiles/r3_e2e_chunks.md); a single layer keeps the library default (8)
+        os.environ.setdefault("NW_HOST_CHUNKS", "4")
 
     import torch
     import torch.distributed as dist

@@ -561,6 +561,8 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
   prm.G = 256 / prm.N;
   if (prm.G > g_cap) prm.G = g_cap;
   if (prm.G < 1) prm.G = 1;
+  // small layers: keep at least two units per SM
+  while (prm.G > 1 && (long long)prm.P * ((prm.nmb + prm.G - 1) / prm.G) < 2 * 148) prm.G /= 2;
   prm.ngrp = (prm.nmb + prm.G - 1) / prm.G;
   if (g.nsh < 1 || g.nsh > kMaxShift) return NW_ERR_UNSUPPORTED;
   prm.nsh = g.nsh;
