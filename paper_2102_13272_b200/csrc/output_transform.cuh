@@ -39,7 +39,10 @@ struct OutCfg {
   // dealt round-robin): 9 warps allow 168 registers per thread, 13 allow 128.  The
   // kernel is latency-bound, so pre-reduced rows (18 instead of 30 values) buy 12
   // consumer warps for the split 12 x 12 tile.
-  static constexpr int CO = (SPL == 1) ? 8 : (SPL == 2 ? 6 : 3);
+#ifndef NW_OUT_CO2
+#define NW_OUT_CO2 6  // measured: 5 -> +7 %, 7 -> +9 % output-transform time on C2
+#endif
+  static constexpr int CO = (SPL == 1) ? 8 : (SPL == 2 ? (PRE ? NW_OUT_CO2 : 6) : 3);
   static constexpr int WARPS = CO * SPL;          // consumer warps
   static constexpr int TS = 32;  // slices per unit (lanes)
   static constexpr int STAGE = RL * CO * TS;        // floats per ring stage
