@@ -445,7 +445,7 @@ def main():
         if world > 1:
             dist.barrier()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ek = max(3, args.steps // 4)
+        ek = max(10, args.steps)
         s0.record(stream)
         for _ in range(ek):
             e2e_chain()
@@ -474,13 +474,13 @@ def main():
 
         for st in streams:
             st.wait_stream(stream)
-        for _ in range(2):
+        for _ in range(3):
             e2e_step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ek = max(3, args.steps // 4)
+        ek = max(10, args.steps)
         s0.record(stream)
         for st in streams:
             st.wait_stream(stream)
