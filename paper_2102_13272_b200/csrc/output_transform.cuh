@@ -18,6 +18,8 @@
 // the instruction cache).  The finished tile goes through a per-warp shared
 // stage so the stores walk output rows across the 32 slices.
 #pragma once
+#include <type_traits>
+
 #include "ptx.cuh"
 #include "transforms.cuh"
 
@@ -277,15 +279,28 @@ __device__ __forceinline__ void out_unit(long long t0, int coe, RowSrc&& rowsrc,
           okw = b >= 0 && q_w < MA && ((kw >> q_w) & 1u) && pw < limw;
         }
         YT* dst = y + (b < 0 ? 0 : b) + pw * colstride;
+        // PReLU and "every tile row inside the image" (warp vote) are resolved once per column
+        // group, so the common store is one predicate, one LDS and one STG per element
+        auto stores = [&](auto prelu_c, auto rows_in_c) {
+          constexpr bool PRELU = decltype(prelu_c)::value, ROWS_IN = decltype(rows_in_c)::value;
 #pragma unroll
-        for (int i = 0; i < HR; ++i) {
-          const int q_h = hph * HR + i;
-          const bool kept = kSimple || ((kh >> q_h) & 1u);
-          if (q_h < MA && okw && kept && OT.pos[q_h < MA ? q_h : 0] < limh) {
-            float v = ptx::lds_f32(ya + i * QW * 4);
-            if (slopes) v = v >= 0.f ? v : slope * v;
-            dst[OT.pos[q_h < MA ? q_h : 0] * rowstride] = from_f<YT>(v);  // 32-bit row offset
+          for (int i = 0; i < HR; ++i) {
+            const int q_h = hph * HR + i;
+            const bool kept = kSimple || ((kh >> q_h) & 1u);
+            if (q_h < MA && okw && kept && (ROWS_IN || OT.pos[q_h < MA ? q_h : 0] < limh)) {
+              float v = ptx::lds_f32(ya + i * QW * 4);
+              if constexpr (PRELU) v = v >= 0.f ? v : slope * v;
+              dst[OT.pos[q_h < MA ? q_h : 0] * rowstride] = from_f<YT>(v);  // 32-bit row offset
+            }
           }
+        };
+        const bool rows_in = __all_sync(0xffffffffu, limh >= MA);
+        if (slopes) {
+          if (rows_in) stores(std::true_type{}, std::true_type{});
+          else stores(std::true_type{}, std::false_type{});
+        } else {
+          if (rows_in) stores(std::false_type{}, std::true_type{});
+          else stores(std::false_type{}, std::false_type{});
         }
       }
       __syncwarp();
