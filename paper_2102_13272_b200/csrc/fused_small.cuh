@@ -22,12 +22,15 @@ struct FusedC1Shape {
   static constexpr int WARPS = CO * SPL;
   static constexpr int THREADS = WARPS * 32;
   static constexpr int P = X::PA * X::PA;
-  static constexpr int VSTR = P | 1;                            // odd slice stride: conflict-free lanes
+  static constexpr int RPV = X::PA + (X::PA & 1);               // V point row padded to float2
+  // slice stride in float2 units odd: conflict-free 64-bit loads across the 32 lanes
+  static constexpr int VSTR = (X::PA * RPV / 2) % 2 ? X::PA * RPV : X::PA * RPV + 2;
   static constexpr int HSTR = X::L | 1;
   static constexpr size_t V_BYTES = (size_t)32 * VSTR * 4;
   static constexpr size_t H_BYTES = (size_t)32 * X::PA * HSTR * 4;  // pass-1 buffer, reused as output stage
   static constexpr size_t STAGE_BYTES = ((size_t)WARPS * O::YST * 4 + 127) / 128 * 128;
-  static constexpr size_t U_BYTES = (size_t)P * CO * 4;
+  static constexpr int RPU = X::PA + (X::PA & 1);               // U point row padded to float2
+  static constexpr size_t U_BYTES = (size_t)CO * X::PA * RPU * 4;
   static constexpr size_t INFO_BYTES = (size_t)WARPS * 32 * 16;
   static constexpr size_t HS_OR_STAGE = H_BYTES > STAGE_BYTES ? H_BYTES : STAGE_BYTES;
   static constexpr size_t SMEM = 128 + V_BYTES + HS_OR_STAGE + U_BYTES + INFO_BYTES;
@@ -97,7 +100,7 @@ __global__ void __launch_bounds__(FusedC1Cfg<MO, RO, MI>::THREADS, 1)
       in_axis<MO, RO, MI>(hin, vv);
 #pragma unroll
       for (int p_w = 0; p_w < PA; ++p_w)
-        Vs[s * C::VSTR + p_h * PA + p_w] = (umode == 2) ? __bfloat162float(__float2bfloat16_rn(vv[p_w])) : vv[p_w];
+        Vs[s * C::VSTR + p_h * C::RPV + p_w] = (umode == 2) ? __bfloat162float(__float2bfloat16_rn(vv[p_w])) : vv[p_w];
     }
     __syncthreads();
     // ---- 2. output channels in groups of CO: rows of M = V (.) U on the fly ----
@@ -114,17 +117,23 @@ __global__ void __launch_bounds__(FusedC1Cfg<MO, RO, MI>::THREADS, 1)
             u = static_cast<const float*>(Uraw)[o];
           }
         }
-        Us[xi * C::CO + cl] = u;
+        Us[(cl * PA + xi / PA) * C::RPU + xi % PA] = u;
       }
       __syncthreads();
       const int coe = co0 + cw_;
       float* yst = Hs + warp * O::YST;
       long long* info = sinfo + warp * 64;
       auto prod_row = [&](int r, float(&mv)[PA]) {
-        const float* vr = Vs + lane * C::VSTR + r * PA;
-        const float* ur = Us + r * PA * C::CO + cw_;
+        // V row of the lane's slice and U row of the warp's channel (broadcast), two points
+        // per 64-bit load
+        const float2* vr = reinterpret_cast<const float2*>(Vs + lane * C::VSTR + r * C::RPV);
+        const float2* ur = reinterpret_cast<const float2*>(Us + (cw_ * PA + r) * C::RPU);
 #pragma unroll
-        for (int p_w = 0; p_w < PA; ++p_w) mv[p_w] = vr[p_w] * ur[p_w * C::CO];
+        for (int k = 0; k < C::RPU / 2; ++k) {
+          const float2 u = ur[k], v = vr[k];
+          mv[2 * k] = v.x * u.x;
+          if (2 * k + 1 < PA) mv[(2 * k + 1) < PA ? 2 * k + 1 : 0] = v.y * u.y;
+        }
       };
       if constexpr (C::SPL == 1) {
         out_unit<MO, RO, MI, YT, false, 0>(t0, coe, prod_row, yst, info, y, g, slopes);
