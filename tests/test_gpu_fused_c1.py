@@ -65,3 +65,35 @@ def test_prelu_bf16_storage_and_plain_bf16():
     _check(layer, "bf16x3", prelu=True)
     _check(layer.with_(dtype="bf16"), "bf16x3", prelu=True)
     _check(layer, "bf16")
+
+
+def test_three_kernel_path_still_matches(tmp_path):
+    # NW_FUSED_C1=0 (read once per process) routes the same layer through input transform,
+    # contraction and output transform; both must agree with each other and the oracle
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import synth\n"
+        "from paper_2102_13272_b200 import NestedConv2d, MATH_BF16X3\n"
+        "l = synth.small(synth.CONFIGS['c5_conv1'], N=2, H=45, W=33)\n"
+        "t = synth.make_inputs(l)\n"
+        "y = NestedConv2d(t['w'].cuda(), 1, l.pad, l.m_o, l.m_i, MATH_BF16X3, outer_taps=l.r_o)(t['x'].cuda())\n"
+        "np.save(%r, y.float().cpu().numpy())\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for flag in ("0", "1"):
+        out = str(tmp_path / f"y{flag}.npy")
+        env = dict(os.environ, NW_FUSED_C1=flag)
+        r = subprocess.run([sys.executable, "-c", code % (root, os.path.join(root, "tests"), out)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[flag] = np.load(out)
+    l = synth.small(BASE, N=2, H=45, W=33)
+    t = synth.make_inputs(l)
+    ref = direct.conv2d(t["x"].double().numpy(), t["w"].double().numpy(), 1, l.pad)
+    for flag, y in outs.items():
+        assert rel_err(y, ref) <= TOL["bf16x3"], flag
+    assert rel_err(outs["0"], outs["1"]) <= TOL["bf16x3"]
