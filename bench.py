@@ -194,6 +194,80 @@ def kernel_work(layer, info, math, path="nested"):
     }
 
 
+def layer_bounds(layer, info, math, peaks, path="nested"):
+    """Per-layer roofline bounds, microseconds.
+
+    compulsory bytes = x + U (or w) + y, each once.  Contraction work of the method:
+      nested  "paper" basis: 625 MACs per 9x9 tile per (cin_e, cout_e) -- the paper's
+              F(3,3)(x)F(3,3) nesting (P:110), i.e. T9 * 625 * Cin_e * Cout_e -- and "plan"
+              basis: the plan's own points (e.g. F(4,3)(x)F(3,3): 900 per 12x12 tile);
+      ola     25 MACs per 3x3 tile per filter block (Eq. 2.3): T3 * 25 * nb^2 * Cin_e * Cout_e;
+      direct  K^2 MACs per output (Eq. 2.1).
+    R1 = max(1-pass contraction at the bf16 burst peak, compulsory bytes at HBM peak);
+    R2 = the same with the passes the math mode issues (bf16x3: 3);
+    R3 = R2's compute term against the path's own algorithmic pipeline bytes (V, M spilled).
+    frac = bound / measured time (filled in by the caller)."""
+    es = 2 if layer.dtype == "bf16" else 4
+    x_b = layer.N * layer.Cin * layer.H * layer.W * es
+    y_b = layer.N * layer.Cout * layer.Ho * layer.Wo * es
+    cin_e, cout_e, Kp = info["cin_e"], info["cout_e"], info["Kp"]
+    if layer.transposed:
+        Hq, Wq = -(-layer.Ho // 2), -(-layer.Wo // 2)
+    else:
+        Hq, Wq = layer.Ho, layer.Wo
+    passes = {"bf16x3": 3, "bf16": 1, "fp32": 1}[math]
+    if math == "fp32":   # CUDA-core FP32 FMA peak: 148 SMs x 128 lanes x 2 x max clock
+        tpeak = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6
+    else:
+        tpeak = peaks["bf16_tflops"] * 1e12
+    if path == "nested":
+        P9 = 625
+        T9 = layer.N * -(-Hq // 9) * -(-Wq // 9)
+        macs = T9 * P9 * cin_e * cout_e
+        adv, nph = info["tile_out"], info["n_phase"]
+        Tp = layer.N * -(-Hq // adv) * -(-Wq // adv) * nph * nph
+        macs_plan = Tp * info["points"] * cin_e * cout_e
+        u_b = info["points"] * cin_e * cout_e * 4
+    elif path == "ola":
+        nb = -(-Kp // 3)
+        T3 = layer.N * -(-Hq // 3) * -(-Wq // 3)
+        macs = macs_plan = T3 * 25 * nb * nb * cin_e * cout_e
+        u_b = 25 * nb * nb * cin_e * cout_e * 4
+    else:
+        macs = macs_plan = layer.direct_flops() // 2
+        u_b = layer.Cin * layer.Cout * layer.K * layer.K * es
+    hbm = peaks["hbm_gbs"] * 1e9
+    comp_b = x_b + u_b + y_b
+    t_b = comp_b / hbm * 1e6
+    t1 = 2 * macs / tpeak * 1e6
+    t2 = 2 * macs * passes / tpeak * 1e6
+    t2_plan = 2 * macs_plan * passes / tpeak * 1e6
+    return {"compulsory_bytes": int(comp_b), "macs_paper_basis": int(macs), "macs_plan": int(macs_plan),
+            "passes": passes, "r1_us": round(max(t1, t_b), 2), "r2_us": round(max(t2, t_b), 2),
+            "r2_plan_us": round(max(t2_plan, t_b), 2), "_t2_compute_us": t2_plan}
+
+
+def attach_bounds(entry, bounds, works_l, peaks, ms):
+    """Add r1/r2/r3 bounds and fractions (bound / measured) to a per-layer entry."""
+    hbm = peaks["hbm_gbs"] * 1e9
+    pipe_b = 0
+    if works_l:
+        pipe_b = sum(v["bytes"] for k, v in works_l.items()
+                     if k not in ("filter_transform", "contraction_fp32_simt"))
+    r3 = max(bounds["_t2_compute_us"], pipe_b / hbm * 1e6) if pipe_b else None
+    us = ms * 1e3
+    rf = {"r1": {"bound_us": bounds["r1_us"], "frac": round(bounds["r1_us"] / us, 4)},
+          "r2": {"bound_us": bounds["r2_us"], "frac": round(bounds["r2_us"] / us, 4),
+                 "basis": "paper F(3,3)(x)F(3,3) MACs x passes at bf16 burst peak vs compulsory x+U+y"},
+          "r2_plan": {"bound_us": bounds["r2_plan_us"], "frac": round(bounds["r2_plan_us"] / us, 4),
+                      "basis": "the plan's own transform points x passes vs compulsory bytes"}}
+    if r3 is not None:
+        rf["r3"] = {"bound_us": round(r3, 2), "frac": round(r3 / us, 4), "pipeline_bytes": int(pipe_b),
+                    "basis": "pipeline bytes (V, M spilled: the implementation's own traffic)"}
+    entry["roofline"] = rf
+    return entry
+
+
 def roofline(prof, works, math, peaks, steps, layers):
     """Pick the kernel with the largest total time; achieved = algorithmic work / mean launch time."""
     if not prof:
@@ -267,6 +341,17 @@ def oracle_sample_time(layers, target_s=10.0, max_images=None):
     return f1, t1, n, np.__version__
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cores_used():
     try:
         return len(os.sched_getaffinity(0))
@@ -275,8 +360,40 @@ def cores_used():
 
 
 # ----------------------------------------------------------------------------
+# multi-GPU launch: one process per GPU
+# ----------------------------------------------------------------------------
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def torchrun_cmd(argv, gpus: int, port: int):
+    """The command that re-runs this script as `gpus` ranks on one node (torch.distributed.run,
+    rendezvous on 127.0.0.1), forwarding every argument."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def ensure_ranks(args) -> None:
+    """`python bench.py --gpus N` with N > 1 and no torchrun environment re-executes itself under
+    torch.distributed.run with N ranks (rank 0 prints the JSON line) and exits with its status.
+    Under torchrun the world size must equal --gpus."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is None:
+        if args.gpus > 1:
+            import subprocess
+            r = subprocess.run(torchrun_cmd(sys.argv[1:], args.gpus, free_port()))
+            sys.exit(r.returncode)
+        return
+    if int(world) != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+
+
 def main():
     args = parse()
+    ensure_ranks(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -300,10 +417,17 @@ def main():
     from paper_2102_13272_b200 import _lib
     from paper_2102_13272_b200 import dist as nwd
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # NW_BENCH_BACKEND=gloo (tests only) runs the multi-rank orchestration on a box with fewer
+    # GPUs than ranks: ranks then share a device, which NCCL refuses; the product run is NCCL
+    backend = os.environ.get("NW_BENCH_BACKEND", "nccl")
+    dev_index = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     math = {"bf16x3": nw.MATH_BF16X3, "fp32": nw.MATH_FP32_SIMT, "bf16": nw.MATH_BF16}[args.math]
     peaks = load_peaks()
     stream = torch.cuda.current_stream()
@@ -311,7 +435,7 @@ def main():
     chain = args.workload in CHAINS
     paths = [("direct" if (chain and l.K <= 3) else args.path) for l in layers_all]
     convs, xs, ys, works = [], [], [], []
-    filt_ms = 0.0
+    filt_ms, bcast_ms, bcast_bytes = 0.0, 0.0, 0
     for li, l in enumerate(layers_all):
         t = synth.make_inputs(l.with_(seed=l.seed + 1000 * rank)) if rank else synth.make_inputs(l)
         if chain and li > 0:
@@ -319,15 +443,23 @@ def main():
         w = synth.make_inputs(l, x=False)["w"].to(dev)     # same weights on every rank
         slopes = torch.full((l.Cout,), synth.PRELU_SLOPE, device=dev) if l.prelu else None
         conv = nw.NestedConv2d(w, l.stride, l.pad, l.m_o, l.m_i, math, transposed=l.transposed, outer_taps=l.r_o,
-                               output_padding=l.output_padding, prelu_slopes=slopes)
-        # filter transform once on rank 0 (timed separately), broadcast U over NCCL
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        conv.transform_filter()
-        e1.record()
-        torch.cuda.synchronize()
-        filt_ms += e0.elapsed_time(e1)
-        nwd.broadcast_filter(conv.U, src=0)   # the one collective: U from rank 0 (NCCL / NVLink)
+                               output_padding=l.output_padding, prelu_slopes=slopes, transform=False)
+        # filter transform once, on rank 0 only (timed separately); the other ranks receive U
+        # through the one collective of the run: a broadcast over NCCL (NVLink / NVSwitch)
+        if rank == 0:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            conv.transform_filter()
+            e1.record()
+            torch.cuda.synchronize()
+            filt_ms += e0.elapsed_time(e1)
+        if world > 1:
+            torch.cuda.synchronize()
+            b0 = time.perf_counter()
+            nwd.broadcast_filter(conv.U, src=0)
+            torch.cuda.synchronize()
+            bcast_ms += (time.perf_counter() - b0) * 1e3
+            bcast_bytes += conv.U.numel()
         x = ys[-1] if (chain and li > 0) else t["x"].to(dev)
         y = torch.empty(conv.out_shape(x.shape), dtype=x.dtype, device=dev)
         conv.workspace(*x.shape[:1], *x.shape[2:], path=paths[li])
@@ -350,7 +482,7 @@ def main():
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = nw.launch_count()
     with ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ
-                      else local) as clk:
+                      else dev_index) as clk:
         _lib.profile_begin()
         torch.cuda.synchronize()
         start.record(stream)
@@ -380,8 +512,16 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         lm = e0.elapsed_time(e1) / reps
-        per_layer.append({"layer": l.name, "path": pth, "ms": round(lm, 4),
-                          "tflops_direct_equiv": round(l.direct_flops() / (lm / 1e3) / 1e12, 2)})
+        ent = {"layer": l.name, "path": pth, "ms": round(lm, 4),
+               "tflops_direct_equiv": round(l.direct_flops() / (lm / 1e3) / 1e12, 2)}
+        per_layer.append(attach_bounds(ent, layer_bounds(l, conv.info, args.math, peaks, pth),
+                                       works[len(per_layer)], peaks, lm))
+
+    # step-level bounds: sum of the layers' bounds over the measured step
+    step_roof = {k: {"bound_us": round(sum(e["roofline"][k]["bound_us"] for e in per_layer if k in e["roofline"]), 2)}
+                 for k in ("r1", "r2", "r2_plan", "r3")}
+    for k, v in step_roof.items():
+        v["frac"] = round(v["bound_us"] / (ms_step * 1e3), 4)
 
     compare = {}
     if not args.no_compare and args.path == "nested" and not chain:
@@ -411,10 +551,33 @@ def main():
                     torch.cuda.synchronize()
                     lm = e0.elapsed_time(e1) / 3
                     tot += lm
-                    lay.append({"layer": l.name, "ms": round(lm, 4), "nested_speedup": round(lm / pl["ms"], 3)})
+                    lmath_name = "bf16" if lmath is not None else args.math
+                    b = layer_bounds(l, conv.info, lmath_name, peaks, path)
+                    wl = kernel_work(l, conv.info, lmath_name, path) if path == "direct" else None
+                    if path == "ola":   # OLA pipeline: F(3,3) V and M per 3x3 tile, U per block
+                        es = 2 if l.dtype == "bf16" else 4
+                        nb = -(-conv.info["Kp"] // 3)
+                        hq = -(-l.Ho // 2) if l.transposed else l.Ho
+                        wq = -(-l.Wo // 2) if l.transposed else l.Wo
+                        T3e = l.N * (-(-hq // 3) + nb - 1) * (-(-wq // 3) + nb - 1)
+                        vb = 25 * T3e * conv.info["cin_e"] * 4
+                        mb = 25 * T3e * conv.info["cout_e"] * 4
+                        xb = l.N * l.Cin * l.H * l.W * es
+                        yb = l.N * l.Cout * l.Ho * l.Wo * es
+                        wl = {"input_transform": {"bytes": xb + vb}, "contraction_tc": {"bytes": vb + mb},
+                              "output_transform": {"bytes": mb + yb}}
+                    ent = {"layer": l.name, "ms": round(lm, 4), "nested_speedup": round(lm / pl["ms"], 3)}
+                    attach_bounds(ent, b, wl, peaks, lm)
+                    # the path's own bound: the slower of its contraction (passes issued) and its
+                    # own pipeline bytes -- what "at its bound" means for this comparison path
+                    own = ent["roofline"].get("r3", ent["roofline"]["r2_plan"])
+                    ent["roofline_frac"] = own["frac"]
+                    lay.append(ent)
                     del conv
+                own_us = sum(e["roofline"].get("r3", e["roofline"]["r2_plan"])["bound_us"] for e in lay)
                 compare[name] = {"ms_per_step": round(tot, 4),
                                  "tflops_direct_equiv": round(flops_rank / (tot / 1e3) / 1e12, 2),
+                                 "roofline_frac": round(own_us / (tot * 1e3), 4),
                                  "per_layer": lay}
                 if lmath is not None:
                     compare[name]["math"] = "bf16"
@@ -498,10 +661,54 @@ def main():
 
     roof = roofline(prof, works, args.math, peaks, args.steps, layers_all)
 
+    # multi-GPU verification (outside every timed region): each rank hashes its outputs; rank 0
+    # regenerates every rank's seeded inputs, runs them through its own U (the broadcast's
+    # source) and must reproduce each rank's hash, i.e. the sharded run equals a 1-rank run
+    # bit for bit
+    multi = None
+    if world > 1:
+        import hashlib
+
+        def digest(tensors):
+            h = hashlib.sha256()
+            for y in tensors:
+                h.update(y.contiguous().view(torch.uint8).cpu().numpy().tobytes())
+            return h.hexdigest()
+
+        step()
+        torch.cuda.synchronize()
+        mine = digest(ys)
+        hashes = [None] * world
+        dist.all_gather_object(hashes, mine)
+        ok = True
+        if rank == 0:
+            for r in range(world):
+                if chain:
+                    xr = synth.make_inputs(layers_all[0].with_(seed=layers_all[0].seed + 1000 * r))["x"] if r \
+                        else synth.make_inputs(layers_all[0])["x"]
+                    xs[0].copy_(xr.to(dev))
+                else:
+                    for l, x in zip(layers_all, xs):
+                        xr = synth.make_inputs(l.with_(seed=l.seed + 1000 * r))["x"] if r else synth.make_inputs(l)["x"]
+                        x.copy_(xr.to(dev))
+                step()
+                torch.cuda.synchronize()
+                ok = ok and digest(ys) == hashes[r]
+        flag = torch.tensor([1 if ok else 0], device=dev)
+        dist.broadcast(flag, src=0)
+        multi = {"bit_identical_to_1_rank": bool(flag.item()), "ranks_checked": world,
+                 "collectives": "one NCCL broadcast of U per layer from rank 0 (outside the timed region); "
+                                "no data-path collective (batch-sharded)",
+                 "u_broadcast_bytes": bcast_bytes, "u_broadcast_ms": round(bcast_ms, 3),
+                 "filter_transform_ranks": [0]}
+        if not ok:
+            print("bench.py: multi-GPU outputs differ from the 1-rank recomputation", file=sys.stderr)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         f, t, n, _ = oracle_sample_time(layers_all, target_s=10.0)
         cpu = {"value": round(f / t / 1e12, 5), "unit": "TFLOP/s", "cores": cores_used(), "kind": "oracle",
+               "cpu_model": cpu_model(),
                "sample": f"oracle.direct FP64 (Eq. 2.1) on {n} image(s) of each layer of the workload "
                          f"({f / 1e9:.1f} GFLOP direct-equivalent in {t:.1f} s)"}
 
@@ -517,13 +724,17 @@ def main():
                                    for c in convs],
                        "path": paths if chain else args.path, "math": args.math,
                        "images_per_rank": layers_all[0].N,
+                       "parallelism": f"dp{world}: batch-sharded, one process per GPU, U broadcast once"
+                                      if world > 1 else "1 GPU",
                        "l2": "no flush: x (>=134 MB) and V/M (>1 GB per layer) exceed the 126 MB L2",
                        "step": "input transform + contraction + output transform per layer (nw_conv_forward)"},
             "images_per_s": round(images, 1),
             "per_layer": per_layer,
             "filter_transform_ms": round(filt_ms, 4),
+            "multi_gpu": multi,
             "compare": compare,
             "roofline": roof,
+            "roofline_step": step_roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -533,6 +744,8 @@ def main():
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if multi is not None and not multi["bit_identical_to_1_rank"]:
+        sys.exit(3)
 
 
 def reference_arm(args, layers, world, rank):
@@ -564,6 +777,7 @@ def reference_arm(args, layers, world, rank):
            "config": {"workload": WORKLOAD_DESC[args.workload], "layers": [l.name for l in layers],
                       "sample": "1 image of each layer per step"},
            "cpu_baseline": {"value": round(v, 5), "unit": "TFLOP/s", "cores": cores_used(), "kind": "oracle",
+                            "cpu_model": cpu_model(),
                             "sample": "oracle.direct FP64 (Eq. 2.1), 1 image of each layer per step"},
            "e2e": {"value": round(v, 5), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)

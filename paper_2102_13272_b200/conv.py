@@ -21,7 +21,10 @@ class NestedConv2d:
 
     def __init__(self, w: torch.Tensor, stride: int = 1, pad: Optional[int] = None, m_outer: int = 3,
                  m_inner: int = 3, math: int = MATH_BF16X3, transposed: bool = False,
-                 output_padding: int = 0, outer_taps: int = 3, prelu_slopes: Optional[torch.Tensor] = None):
+                 output_padding: int = 0, outer_taps: int = 3, prelu_slopes: Optional[torch.Tensor] = None,
+                 transform: bool = True):
+        """transform=False allocates U without computing it: a multi-GPU run transforms the
+        filter on rank 0 only and broadcasts U (dist.broadcast_filter) into the other ranks'."""
         if not w.is_cuda:
             raise ValueError("w must be a CUDA tensor")
         if w.dtype not in _DT:
@@ -38,7 +41,8 @@ class NestedConv2d:
         self.Cin, self.Cout = Cin, Cout
         self.U = torch.empty(self.info["filter_bytes"], dtype=torch.uint8, device=w.device)
         self._ws = {}
-        self.transform_filter()
+        if transform:
+            self.transform_filter()
 
     def transform_filter(self, stream=None) -> None:
         self.plan.transform_filter(self.w, self.U, stream)
@@ -59,12 +63,23 @@ class NestedConv2d:
                  stream=None) -> torch.Tensor:
         if x.dtype != self.dtype or not x.is_cuda:
             raise ValueError("x must be a CUDA tensor with the filter's dtype")
+        if x.device != self.w.device:
+            raise ValueError(f"x is on {x.device}, the plan's filter on {self.w.device}")
+        if x.dim() != 4:
+            raise ValueError("x must be NCHW")
         x = x.contiguous()
         N, C, H, W = x.shape
         if C != self.Cin:
             raise ValueError("channel mismatch")
         if y is None:
             y = torch.empty(self.out_shape(x.shape), dtype=self.dtype, device=x.device)
+        else:  # the C ABI writes through a raw pointer: shape, dtype, device and layout must match
+            if tuple(y.shape) != self.out_shape(x.shape):
+                raise ValueError(f"y has shape {tuple(y.shape)}, expected {self.out_shape(x.shape)}")
+            if y.dtype != self.dtype or y.device != x.device:
+                raise ValueError("y must have the filter's dtype and x's device")
+            if not y.is_contiguous():
+                raise ValueError("y must be contiguous (NCHW)")
         ws = self.workspace(N, H, W, path)
         if path == "nested":
             self.plan.forward(x, self.U, y, N, H, W, ws, ws.numel(), stream)

@@ -27,6 +27,16 @@ nw_status_t nw_transform_filter(nw_plan_t p, const void *w, void *U, nw_stream_t
 
 namespace nw {
 
+// grow a plan's event pool to n events (caller holds the pool's mutex)
+static bool ensure_events(std::vector<cudaEvent_t> &pool, size_t n) {
+  while (pool.size() < n) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return false;
+    pool.push_back(e);
+  }
+  return true;
+}
+
 static int env_int(const char *name, int dflt) {
   const char *v = getenv(name);
   return (v && *v) ? atoi(v) : dflt;
@@ -112,16 +122,15 @@ nw_status_t nw_conv_forward(nw_plan_t p, const void *x, const void *U, void *y, 
   const size_t vb = v_bytes(p, gc), mb = m_bytes(p, gc);
   const size_t es = (p->dtype == NW_DTYPE_BF16) ? 2 : 4;
   const size_t ximg = (size_t)p->Cin * H * W * es, yimg = (size_t)p->Cout * gfull.Ho * gfull.Wo * es;
-  {
-    std::lock_guard<std::mutex> lk(p->io_mu);
-    for (auto &ps : p->s_pipe)
-      if (!ps && cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking) != cudaSuccess) return NW_ERR_CUDA;
-  }
+  // streams and events of the pipeline (the plan's, created once; enqueued under pipe_mu,
+  // which nw_conv_forward_host's io_mu nests around)
+  std::lock_guard<std::mutex> lk(p->pipe_mu);
+  for (auto &ps : p->s_pipe)
+    if (!ps && cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking) != cudaSuccess) return NW_ERR_CUDA;
   cudaStream_t si = p->s_pipe[0], sg = p->s_pipe[1], so = p->s_pipe[2];
   // events: start, then per chunk in / gemm / out
-  std::vector<cudaEvent_t> ev(1 + 3 * (size_t)nchunks, nullptr);
-  for (auto &e : ev)
-    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return NW_ERR_CUDA;
+  if (!ensure_events(p->ev_pipe, 1 + 3 * (size_t)nchunks)) return NW_ERR_CUDA;
+  const std::vector<cudaEvent_t> &ev = p->ev_pipe;
   auto E_in = [&](int c) { return ev[1 + 3 * c]; };
   auto E_gemm = [&](int c) { return ev[2 + 3 * c]; };
   auto E_out = [&](int c) { return ev[3 + 3 * c]; };
@@ -143,7 +152,6 @@ nw_status_t nw_conv_forward(nw_plan_t p, const void *x, const void *U, void *y, 
     ok = ok && cudaEventRecord(E_out(c), so) == cudaSuccess;
   }
   if (ok && st == NW_OK) ok = cudaStreamWaitEvent(s, E_out(nchunks - 1), 0) == cudaSuccess;
-  for (auto &e : ev) cudaEventDestroy(e);
   if (st != NW_OK) return st;
   return ok ? NW_OK : NW_ERR_CUDA;
 }
@@ -177,6 +185,8 @@ static void host_layout(const nw_plan_st *p, int N, int H, int W, size_t *fw, si
 }
 
 nw_plan_st::~nw_plan_st() {
+  for (auto e : ev_host) cudaEventDestroy(e);
+  for (auto e : ev_pipe) cudaEventDestroy(e);
   if (s_h2d) cudaStreamDestroy(s_h2d);
   if (s_d2h) cudaStreamDestroy(s_d2h);
   for (auto &ps : s_pipe)
@@ -213,11 +223,9 @@ nw_status_t nw_conv_forward_host(nw_plan_t p, const void *x_host, const void *U,
   char *xd[2] = {base + fw, base + fw + xb};
   char *yd[2] = {base + fw + 2 * xb, base + fw + 2 * xb + yb};
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  {
-    std::lock_guard<std::mutex> lk(p->io_mu);
-    if (!p->s_h2d && cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking) != cudaSuccess) return NW_ERR_CUDA;
-    if (!p->s_d2h && cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking) != cudaSuccess) return NW_ERR_CUDA;
-  }
+  std::lock_guard<std::mutex> lk(p->io_mu);  // copy streams and the event pool (enqueue only)
+  if (!p->s_h2d && cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking) != cudaSuccess) return NW_ERR_CUDA;
+  if (!p->s_d2h && cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking) != cudaSuccess) return NW_ERR_CUDA;
   // chunk schedule: ramp 1, 2, 4 .. up to nc images, nc-image chunks, ramp back down, so the
   // unoverlapped first copy in and last copy out are one image each
   std::vector<int> sizes;
@@ -235,10 +243,10 @@ nw_status_t nw_conv_forward_host(nw_plan_t p, const void *x_host, const void *U,
     }
   }
   const int nchunks = (int)sizes.size();
-  // events: [0] start, per chunk: in (x landed), comp (forward done), out (y copied)
-  std::vector<cudaEvent_t> ev(1 + 3 * (size_t)nchunks, nullptr);
-  for (auto &e : ev)
-    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return NW_ERR_CUDA;
+  // events: [0] start, per chunk: in (x landed), comp (forward done), out (y copied); the
+  // plan's pool, enqueued under io_mu
+  if (!ensure_events(p->ev_host, 1 + 3 * (size_t)nchunks)) return NW_ERR_CUDA;
+  const std::vector<cudaEvent_t> &ev = p->ev_host;
   auto E_in = [&](int k) { return ev[1 + 3 * k]; };
   auto E_comp = [&](int k) { return ev[2 + 3 * k]; };
   auto E_out = [&](int k) { return ev[3 + 3 * k]; };
@@ -262,7 +270,6 @@ nw_status_t nw_conv_forward_host(nw_plan_t p, const void *x_host, const void *U,
     ok = ok && cudaEventRecord(E_out(k), p->s_d2h) == cudaSuccess;
   }
   if (st == NW_OK && ok) ok = cudaStreamWaitEvent(s, E_out(nchunks - 1), 0) == cudaSuccess;
-  for (auto &e : ev) cudaEventDestroy(e);  // released once their work completes
   if (st != NW_OK) return st;
   return ok ? NW_OK : NW_ERR_CUDA;
 }

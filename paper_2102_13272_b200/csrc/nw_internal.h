@@ -6,6 +6,7 @@
 #include <atomic>
 #include <mutex>
 #include <utility>
+#include <vector>
 #include <cstddef>
 #include <cstdint>
 
@@ -68,6 +69,11 @@ struct nw_plan_st {
   // streams of the chunk pipeline inside nw_conv_forward (input / contraction / output)
   cudaStream_t s_pipe[3] = {nullptr, nullptr, nullptr};
   int pipe_chunks = -1;  // batch chunks of the forward pipeline (-1: NW_PIPE_CHUNKS or the default)
+  // ordering events of nw_conv_forward_host / the chunk pipeline, created once and reused:
+  // the host path enqueues under io_mu, the pipeline under pipe_mu (a stream wait captures the
+  // event's latest record when it is enqueued, so re-recording by a later call is safe)
+  std::mutex pipe_mu;
+  std::vector<cudaEvent_t> ev_host, ev_pipe;
   ~nw_plan_st();
 };
 

@@ -602,7 +602,9 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
     const char* v = getenv("NW_CLUSTER");
     return v ? atoi(v) : 2;
   }();
-  const int CL = (cl_env == 2 && prm.G == 1 && prm.nmb >= 2 && g.nsh == 1 && prm.N % 16 == 0) ? 2 : 1;
+  // pairs need two CTAs: a grid cap below 2 (NW_GEMM_CTAS=1 in the chunk pipeline) runs unpaired
+  const int CL = (cl_env == 2 && prm.G == 1 && prm.nmb >= 2 && g.nsh == 1 && prm.N % 16 == 0 &&
+                  (g.gemm_ctas <= 0 || g.gemm_ctas >= 2)) ? 2 : 1;
   if (CL > 1) prm.ngrp = (prm.nmb + CL - 1) / CL;
   if (!make_map(&mapU, U, rowsU, (long long)g.nsh * g.cin_pad, prm.N / CL, prm.kbk)) return NW_ERR_CUDA;
   if (CL > 1 ? ensure_smem<tc::contraction_kernel<2>>(227 * 1024) != NW_OK

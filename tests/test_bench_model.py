@@ -35,3 +35,23 @@ def test_single_kernel_layers_and_roofline_pick():
         prof = {k: (len(layers), 1.0 + i) for i, k in enumerate(sorted(kinds))}
         r = bench.roofline(prof, works, "bf16x3", peaks, 1, layers)
         assert r["frac"] > 0 and r["kernel"] in kinds
+
+
+def test_multi_gpu_launch_command(monkeypatch):
+    # `bench.py --gpus N` without a torchrun environment re-executes itself as N ranks on one node
+    cmd = bench.torchrun_cmd(["--gpus", "4", "--steps", "3"], 4, 29555)
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=29555" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "3"] and cmd[-5].endswith("bench.py")
+
+    class A:
+        gpus = 2
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    import pytest
+    with pytest.raises(SystemExit):
+        bench.ensure_ranks(A())          # torchrun world size must match --gpus
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    bench.ensure_ranks(A())              # consistent: runs in this process
+    monkeypatch.delenv("WORLD_SIZE")
+    A.gpus = 1
+    bench.ensure_ranks(A())              # single GPU: no re-exec

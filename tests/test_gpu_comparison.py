@@ -11,7 +11,7 @@ import torch
 
 import synth
 from oracle.errstudy import rel_err
-from test_gpu_nested import SMALL, TOL, _math, _ref
+from test_gpu_nested import SMALL, TOL, _math, _ref, check_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -36,12 +36,7 @@ def test_comparison_path_parity(name, math, path):
     layer = SMALL[name]
     t, y = _run(layer, math, path)
     ref = _ref(layer, t)
-    assert y.shape == ref.shape
-    tol = TOL[math]
-    if layer.dtype == "bf16":
-        tol = max(tol, 2.0 ** -8)   # bf16 output storage adds <= 2^-9 relative
-    err = rel_err(y, ref)
-    assert np.isfinite(y).all() and err <= tol, err
+    check_parity(y, ref, math, layer.dtype)
 
 
 @pytest.mark.parametrize("N,H,W", [(1, 1, 1), (2, 10, 37), (1, 64, 5)])

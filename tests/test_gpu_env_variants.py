@@ -1,0 +1,97 @@
+"""Off-default code paths selected by environment tunables (include/nw.h), each run in a
+fresh process (the library reads them once) and compared with the default path.
+
+Tunables that only change scheduling (chunking, CTA pairs, K-block width, unit size,
+launch mode, channels per CTA) must give BIT-IDENTICAL outputs: every output is the
+same sequence of fp32 operations.  Tunables that change the arithmetic (NW_FUSE_AI=0:
+the inner output level leaves the contraction epilogue; NW_FUSED_C1=0: the three-kernel
+pipeline instead of the single fused kernel) are checked against the FP64 oracle with the
+BASELINE gate.  Also the bench's end-to-end configuration: nw_conv_forward_host at N = 32
+with NW_HOST_CHUNKS=4 (chunk schedule 1,2,4,8,8,4,2,1... with a short tail) bit for bit
+against the device entry point.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import synth
+from test_gpu_nested import _ref, check_parity
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _run(spec, env=None, host=False, tmp=None):
+    out = os.path.join(str(tmp), f"y_{abs(hash((json.dumps(spec, sort_keys=True), json.dumps(env), host)))}.npy")
+    e = dict(os.environ)
+    e.update(env or {})
+    cmd = [sys.executable, os.path.join(HERE, "_variant_run.py"), json.dumps(spec), out] + (["host"] if host else [])
+    r = subprocess.run(cmd, env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return np.load(out)
+
+
+C2 = {"config": "c2k9", "N": 3, "H": 47, "W": 53, "Cin": 64, "Cout": 64}
+C3 = {"config": "c3", "N": 2, "H": 40, "W": 37, "Cin": 64, "Cout": 256}
+C4B = {"config": "c4b", "N": 3, "H": 45, "W": 40, "Cin": 16, "Cout": 32}
+
+BITWISE = [
+    (C2, {"NW_PIPE_CHUNKS": "2"}),
+    (C2, {"NW_PIPE_CHUNKS": "3"}),            # N = 3 over 3 chunks; with N = 5 below a short tail
+    ({**C2, "N": 5}, {"NW_PIPE_CHUNKS": "3"}),
+    (C2, {"NW_PDL": "1"}),
+    (C2, {"NW_KBK": "64"}),
+    (C2, {"NW_IN_CC": "16"}),
+    (C2, {"NW_IN_CC": "64"}),
+    (C3, {"NW_CLUSTER": "1"}),
+    (C3, {"NW_GEMM_G": "1"}),
+    (C3, {"NW_PDL": "1"}),
+    (C4B, {"NW_KBK": "64"}),
+    (C4B, {"NW_PIPE_CHUNKS": "2"}),
+    (C3, {"NW_PIPE_CHUNKS": "2", "NW_GEMM_CTAS": "1"}),   # grid cap below a CTA pair: unpaired launch
+]
+
+
+@pytest.mark.parametrize("spec,env", BITWISE, ids=[f"{s['config']}-{'-'.join(f'{k}={v}' for k, v in e.items())}"
+                                                   for s, e in BITWISE])
+def test_scheduling_tunables_bit_identical(spec, env, tmp_path):
+    y0 = _run(dict(spec), None, tmp=tmp_path)
+    y1 = _run(dict(spec), env, tmp=tmp_path)
+    assert y0.shape == y1.shape
+    assert np.array_equal(y0, y1), float(np.abs(y0 - y1).max())
+
+
+ARITH = [
+    (C2, {"NW_FUSE_AI": "0"}),
+    ({"config": "c5_conv1", "N": 2, "H": 37, "W": 45}, {"NW_FUSED_C1": "0"}),
+]
+
+
+@pytest.mark.parametrize("spec,env", ARITH, ids=["fuse_ai_off", "fused_c1_off"])
+def test_arithmetic_tunables_meet_gate(spec, env, tmp_path):
+    y = _run(dict(spec), env, tmp=tmp_path)
+    s = dict(spec)
+    layer = synth.small(synth.CONFIGS[s.pop("config")], **s)
+    check_parity(y, _ref(layer, synth.make_inputs(layer)), "bf16x3", layer.dtype)
+
+
+def test_bench_e2e_configuration_bit_identical(tmp_path):
+    # bench.py's e2e leg: full C2 K=9 (N = 32) through nw_conv_forward_host with NW_HOST_CHUNKS=4
+    spec = {"config": "c2k9"}
+    y_dev = _run(dict(spec), None, tmp=tmp_path)
+    y_host = _run(dict(spec), {"NW_HOST_CHUNKS": "4"}, host=True, tmp=tmp_path)
+    assert np.array_equal(y_dev, y_host)
+
+
+@pytest.mark.parametrize("chunks,N", [("3", 7), ("5", 11)])
+def test_host_chunk_schedules_bit_identical(chunks, N, tmp_path):
+    # ramp 1, 2, .. / full chunks / short tail / ramp down, with N not a multiple of the chunk
+    spec = {**C2, "N": N, "Cin": 32, "Cout": 32}
+    y_dev = _run(dict(spec), None, tmp=tmp_path)
+    y_host = _run(dict(spec), {"NW_HOST_CHUNKS": chunks}, host=True, tmp=tmp_path)
+    assert np.array_equal(y_dev, y_host)

@@ -77,3 +77,33 @@ def test_host_entry_point_matches_device(N):
     conv.plan.forward_host(hx, conv.U, hy, N, layer.H, layer.W, ws, nbytes)
     torch.cuda.synchronize()
     assert torch.equal(hy, y_dev)
+
+
+# ---------------------------------------------------------------------------
+# Full-tensor parity at the full BASELINE sizes (every output, both math modes).
+# The FP64 oracle (oracle.direct, einsum per tap) runs on all host cores: C2
+# ~5 s per layer, C3 ~40 s on a 16-core host.  One reference per layer serves
+# both math modes.
+# ---------------------------------------------------------------------------
+FULL_TENSOR = ["c2k5", "c2k7", "c2k9", "c3", "c4a", "c4b", "c5_conv1", "c5_deconv"]
+
+
+@pytest.mark.parametrize("name", FULL_TENSOR)
+def test_full_size_full_tensor(name):
+    from paper_2102_13272_b200 import NestedConv2d
+    from test_gpu_nested import _ref, check_parity
+    layer = synth.CONFIGS[name]
+    t = synth.make_inputs(layer)
+    ref = _ref(layer, t)
+    x, w = t["x"].cuda(), t["w"].cuda()
+    slopes = torch.full((layer.Cout,), synth.PRELU_SLOPE, device="cuda") if layer.prelu else None
+    errs = {}
+    for math in ("bf16x3", "fp32"):
+        conv = NestedConv2d(w, layer.stride, layer.pad, layer.m_o, layer.m_i, _math(math), outer_taps=layer.r_o,
+                            transposed=layer.transposed, output_padding=layer.output_padding, prelu_slopes=slopes)
+        y = conv(x)
+        torch.cuda.synchronize()
+        errs[math] = check_parity(y.float().cpu().numpy(), ref, math, layer.dtype)
+        del conv, y
+        torch.cuda.empty_cache()
+    print(name, {k: f"{v:.3e}" for k, v in errs.items()})

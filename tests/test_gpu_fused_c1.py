@@ -11,6 +11,7 @@ import torch
 import synth
 from oracle import direct
 from oracle.errstudy import rel_err
+from test_gpu_nested import check_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -37,9 +38,10 @@ def _check(layer, math, prelu=False):
     ref = direct.conv2d(t["x"].double().numpy(), t["w"].double().numpy(), layer.stride, layer.pad)
     if prelu:
         ref = np.where(ref >= 0, ref, slope * ref)
-    tol = TOL[math] if layer.dtype == "f32" else max(TOL[math], 2.0 ** -8)
-    assert np.isfinite(y).all()
-    assert rel_err(y, ref) <= tol
+    if math == "bf16":
+        assert np.isfinite(y).all() and rel_err(y, ref) <= TOL[math]
+    else:
+        check_parity(y, ref, math, layer.dtype)
 
 
 BASE = synth.CONFIGS["c5_conv1"]

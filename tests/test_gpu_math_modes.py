@@ -6,7 +6,7 @@ import pytest
 
 from oracle.errstudy import rel_err
 from test_gpu_comparison import _run
-from test_gpu_nested import SMALL, TOL, _ref
+from test_gpu_nested import SMALL, TOL, _ref, check_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -28,5 +28,4 @@ def test_direct_path_meets_gate_in_plain_bf16(name):
     # bench.py's direct_bf16 comparison leg: the direct path's cheapest mode passing the 5e-3 gate
     layer = SMALL[name]
     t, y = _run(layer, "bf16", "direct")
-    tol = TOL["bf16x3"] if layer.dtype == "f32" else max(TOL["bf16x3"], 2.0 ** -8)
-    assert rel_err(y, _ref(layer, t)) <= tol
+    check_parity(y, _ref(layer, t), "bf16x3", layer.dtype)

@@ -24,3 +24,14 @@ def test_split_reconstructs():
     hi, lo = split_bf16(a)
     assert np.all(np.abs((hi.astype(np.float64) + lo) - a) <= np.abs(a) * 2.0 ** -16)
     assert rel_err([1.0, 2.0], [1.0, 2.0]) == 0.0
+
+
+def test_rel_err_hand_computed():
+    # max|y - ref| / max|ref|: |diffs| = (0, 0.5, 1), max|ref| = 4 -> 0.25 (R14)
+    assert rel_err([1.0, 2.5, -3.0], [1.0, 2.0, -4.0]) == 0.25
+    # the denominator is the max over the reference, not over y, and signs count
+    assert rel_err([-1.0, -2.0], [1.0, 2.0]) == 2.0
+    assert rel_err(np.zeros((2, 3)), np.full((2, 3), -0.5)) == 1.0
+    # 2-D / 4-D inputs reduce over every element
+    y = np.zeros((2, 2, 2, 2)); r = np.ones((2, 2, 2, 2)); y[1, 0, 1, 1] = 1.75; r[0, 1, 0, 0] = 8.0
+    assert rel_err(y, r) == 8.0 / 8.0
