@@ -38,9 +38,11 @@
  *    call or workspace query, so sizes stay consistent); NW_PDL=1 launches the
  *    three hot kernels with programmatic dependent launch; NW_FUSED_C1=0 turns
  *    off the single-kernel path for one-input-channel layers; NW_CLUSTER=1
- *    disables the CTA pairs (B multicast) of the plain contraction; NW_GEMM_G=g
+ *    disables the CTA pairs (B multicast) of the plain contraction; NW_INPUT_TMA=0 selects
+ *    the first-round input transform instead of the persistent TMA-fed kernel; NW_GEMM_G=g
  *    caps its 128-slice blocks per unit (default 16); NW_KBK=64 forces 64-wide
- *    K blocks for narrow layers (default: 16 / 32 when cin_pad is 16 / 32).
+ *    K blocks for narrow layers (default: 16 / 32 when cin_pad is 16 / 32);
+ *    NW_DEBUG_SYNC=1 synchronises after every launch and names a faulting kernel on stderr.
  */
 #ifndef NW_H_
 #define NW_H_

@@ -39,16 +39,30 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+def _stale(src: str, headers_mtime: float) -> bool:
+    """An object is rebuilt when its .cu, any header (.cuh / .h, incl. include/nw.h) or this
+    script is newer than it (headers are shared by most translation units)."""
+    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    return os.path.getmtime(os.path.join(CSRC, src)) > t or headers_mtime > t
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every csrc/*.cu to an object and link libnw.so; skipped when up to date."""
+    """Compile the stale csrc/*.cu objects and link libnw.so; skipped when up to date."""
     os.makedirs(BUILD, exist_ok=True)
     hdr = os.path.join(os.path.dirname(HERE), "include", "nw.h")
     newest = max(_deps_mtime(), os.path.getmtime(hdr), os.path.getmtime(__file__))
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
         return LIB
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    hmt = max([os.path.getmtime(h) for h in headers] + [os.path.getmtime(hdr), os.path.getmtime(__file__)])
     srcs = sources()
-    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
+    todo = srcs if force else [s for s in srcs if _stale(s, hmt)]
+    with cf.ThreadPoolExecutor(max_workers=max(1, min(16, len(todo)))) as ex:
+        list(ex.map(lambda s: _compile(s, verbose), todo))
+    objs = [os.path.join(BUILD, s.replace(".cu", ".o")) for s in srcs]
     cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -6,6 +6,11 @@ namespace nw {
 // ---------------------------------------------------------------------------
 // G3s: FP32 SIMT contraction, batched over transform points
 // M[xi][co][t] = sum_k V[xi][t][k] * U[xi][co][k]
+// The channel sum is accumulated in FP64: the product of two fp32 operands is exact in fp64,
+// so M carries one rounding (to fp32, at the store) instead of one per channel.  With fp32
+// accumulation the FP32 path measured 1.12e-4 on C3 at full size (Cin = 256, nested
+// F(4,3) (x) F(3,3): the output transform amplifies the M rounding), above the 1e-4 gate;
+// a CPU split of the error (fp32 V / U / M separately) put 90 % of it in the accumulation.
 // ---------------------------------------------------------------------------
 struct Shifts {
   int nsh, cin_pad;
@@ -25,7 +30,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
   const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
   const float* Vb = V + (long long)xi * T_pad * sh.cin_pad;
   const float* Ub = U + ((long long)xi * Nn + n0) * K;
-  float acc[4][4] = {};
+  double acc[4][4] = {};
   const int lr = tid / 4, lk = (tid % 4) * 4;
   for (int k0 = 0; k0 < K; k0 += 16) {
     const int s = k0 / sh.cin_pad, kc = k0 - s * sh.cin_pad;
@@ -47,7 +52,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma((double)ar[i], (double)br[j], acc[i][j]);
     }
     __syncthreads();
   }
@@ -57,7 +62,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
     const int co = n0 + tx * 4 + j;
     if (co < Nn) {
       float* dst = M + ((long long)xi * Nn + co) * T_pad + t0 + ty * 4;
-      *reinterpret_cast<float4*>(dst) = make_float4(acc[0][j], acc[1][j], acc[2][j], acc[3][j]);
+      *reinterpret_cast<float4*>(dst) =
+          make_float4((float)acc[0][j], (float)acc[1][j], (float)acc[2][j], (float)acc[3][j]);
     }
   }
 }

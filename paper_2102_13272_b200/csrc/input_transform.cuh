@@ -102,6 +102,12 @@ __device__ __forceinline__ void store_row_imm(const float (*za)[Ax<MO, RO, MI>::
   }
 }
 
+}  // namespace nw
+
+#include "input_transform_tma.cuh"  // persistent TMA-fed kernel (uses store_row_imm)
+
+namespace nw {
+
 template <int MO, int RO, int MI, int SR, int CC, typename XT, bool BF, int CINP>
 __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, RO, MI, SR, CC>::MINB)
     input_transform_kernel(const XT* __restrict__ x, void* __restrict__ Vout,
@@ -303,6 +309,13 @@ static nw_status_t input_launch_c(const Geometry& g, const void* x, void* V, cud
 // compile-time channel pitch for the common blocked layouts (immediate store offsets)
 template <int MO, int RO, int MI, int SR, int CC, typename XT, bool BF>
 static nw_status_t input_launch(const Geometry& g, const void* x, void* V, cudaStream_t s) {
+  if constexpr (BF && SR == 1 && Ax<MO, RO, MI>::NPH == 1) {  // persistent TMA kernel (input_transform_tma.cuh)
+    if (input_tma_eligible<MO, RO, MI, XT>(g)) {
+      if (g.cin_pad == 64) return input_tma_launch<MO, RO, MI, XT, 64>(g, x, V, s);
+      if (g.cin_pad == 256) return input_tma_launch<MO, RO, MI, XT, 256>(g, x, V, s);
+      if (g.cin_pad == 32) return input_tma_launch<MO, RO, MI, XT, 32>(g, x, V, s);
+    }
+  }
   if constexpr (BF && SR == 1) {
     if (g.vblk && g.cin_pad == 64) return input_launch_c<MO, RO, MI, SR, CC, XT, BF, 64>(g, x, V, s);
     if (g.vblk && g.cin_pad == 256) return input_launch_c<MO, RO, MI, SR, CC, XT, BF, 256>(g, x, V, s);

@@ -4,6 +4,9 @@
 #include <mutex>
 #include <vector>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "nw_internal.h"
 
 namespace nw {
@@ -38,7 +41,21 @@ LaunchScope::LaunchScope(const char *kind, cudaStream_t s) : kind_(kind), s_(s) 
   cudaEventRecord(a_, s_);
 }
 
+// NW_DEBUG_SYNC=1 (diagnostics only): synchronise after every library launch and name the
+// kernel kind on stderr if it faulted.
+static bool debug_sync() {
+  static const bool on = [] {
+    const char *v = getenv("NW_DEBUG_SYNC");
+    return v && atoi(v) != 0;
+  }();
+  return on;
+}
+
 LaunchScope::~LaunchScope() {
+  if (debug_sync()) {
+    const cudaError_t e = cudaStreamSynchronize(s_);
+    if (e != cudaSuccess) fprintf(stderr, "[nw] kernel %s: %s\n", kind_, cudaGetErrorString(e));
+  }
   if (!a_) return;
   cudaEventRecord(b_, s_);
   std::lock_guard<std::mutex> lk(g_mu);

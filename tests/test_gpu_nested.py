@@ -215,3 +215,24 @@ def test_output_buffer_is_validated():
         conv(t["x"])   # host x
     y = torch.empty(shp, device="cuda")
     assert conv(x, y) is y
+
+
+# the persistent TMA-fed input transform (input_transform_tma.cuh) runs where x rows are
+# 16-byte multiples; these shapes take it, with more tasks than two per CTA (in-loop TMA
+# refills), every 16-byte phase of the window start and ragged tile edges
+TMA_SHAPES = {
+    "c2k9": synth.small(synth.CONFIGS["c2k9"], N=8, H=61, W=64),
+    "c2k5": synth.small(synth.CONFIGS["c2k5"], N=4, H=50, W=76),
+    "c2k7": synth.small(synth.CONFIGS["c2k7"], N=3, H=47, W=92),
+    "c3": synth.small(synth.CONFIGS["c3"], N=3, H=40, W=48, Cin=64, Cout=64),
+    "c5_deconv": synth.small(synth.CONFIGS["c5_deconv"], N=2, H=30, W=44),
+    "c2k9_m3": synth.small(synth.CONFIGS["c2k9"], N=4, H=45, W=60).with_(m_o=3),
+}
+
+
+@pytest.mark.parametrize("math", ["bf16x3"])
+@pytest.mark.parametrize("name", list(TMA_SHAPES))
+def test_tma_input_transform_shapes(name, math):
+    layer = TMA_SHAPES[name]
+    t, y = _run(layer, math)
+    check_parity(y, _ref(layer, t), math, layer.dtype)
