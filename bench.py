@@ -47,7 +47,8 @@ CHAINS = {"c5net"}
 WORKLOAD_DESC = {
     "c5net": "configs[4] as a network: conv5x5 1->32 +PReLU (nested) -> 1x1 32->5 -> 3x3 5->5 -> 1x1 5->32 "
              "(+PReLU each, direct implicit GEMM) -> 9x9 s2 deconv 32->1 (nested), N=16, 540x960 -> 1080x1920",
-    "table1": "paper Table I conv2d shapes (P:154-160): SRCNN 9x9 64<-1, 5x5 32<-64, 5x5 1<-32, 256x256, N=8, fp32",
+    "table1": "paper Table I shapes (P:154-160): SRCNN 9x9 64<-1, PNASNet depthwise 7x7 54 (83x83), "
+              "SRCNN 5x5 32<-64, 5x5 1<-32 (256x256), N=8, fp32",
     "c1": "configs[0]: 5x5 s1 p2, N=1, Cin=Cout=16, 32x32, fp32, F(2,3)(x)F(2,3) + coverage phases",
     "c2": "configs[1]: filter-size sweep K in {5,7,9}, s1 same pad, N=32, Cin=Cout=64, 128x128, fp32",
     "c3": "configs[2]: 9x9 s1 p4, N=64, Cin=Cout=256, 64x64, bf16 storage, fp32 accumulate",
@@ -180,6 +181,16 @@ def kernel_work(layer, info, math, path="nested"):
     u_b = P * cout_e * cin_e * 4
     passes = {"bf16x3": 3, "bf16": 1, "fp32": 1}[math]
     flops = 2 * P * T * cin_e * cout_e
+    if layer.depthwise:
+        # depthwise (groups = C): no channel contraction; the per-channel product kernel reads V
+        # and U and writes M (csrc/depthwise.cu), HBM-bound
+        u_b = P * cout_e * 4
+        return {
+            "input_transform": {"bytes": x_b + v_b, "flops": 0},
+            "depthwise_product": {"bytes": v_b + u_b + m_b, "flops": 0},
+            "output_transform": {"bytes": m_b + y_b, "flops": 0},
+            "filter_transform": {"bytes": u_b, "flops": 0},
+        }
     if info.get("single_kernel"):
         # one input channel: transform, pointwise product and output transform in one kernel;
         # HBM traffic is x, U and y only (the kernel is bound by its CUDA-core transforms)
@@ -211,6 +222,8 @@ def layer_bounds(layer, info, math, peaks, path="nested"):
     x_b = layer.N * layer.Cin * layer.H * layer.W * es
     y_b = layer.N * layer.Cout * layer.Ho * layer.Wo * es
     cin_e, cout_e, Kp = info["cin_e"], info["cout_e"], info["Kp"]
+    if layer.depthwise:   # one product per channel: the "contraction" has Cin_e x Cout_e -> C
+        cin_e = 1
     if layer.transposed:
         Hq, Wq = -(-layer.Ho // 2), -(-layer.Wo // 2)
     else:
@@ -235,7 +248,7 @@ def layer_bounds(layer, info, math, peaks, path="nested"):
         u_b = 25 * nb * nb * cin_e * cout_e * 4
     else:
         macs = macs_plan = layer.direct_flops() // 2
-        u_b = layer.Cin * layer.Cout * layer.K * layer.K * es
+        u_b = (1 if layer.depthwise else layer.Cin) * layer.Cout * layer.K * layer.K * es
     hbm = peaks["hbm_gbs"] * 1e9
     comp_b = x_b + u_b + y_b
     t_b = comp_b / hbm * 1e6
@@ -329,6 +342,8 @@ def oracle_sample_time(layers, target_s=10.0, max_images=None):
             for _ in range(n_img):
                 if l.transposed:
                     direct.conv_transpose2d(x, w, l.stride, l.pad, l.output_padding)
+                elif l.depthwise:
+                    direct.conv2d_depthwise(x, w, l.stride, l.pad)
                 else:
                     direct.conv2d(x, w, l.stride, l.pad)
             flops += n_img * l.with_(N=1).direct_flops()
@@ -443,7 +458,8 @@ def main():
         w = synth.make_inputs(l, x=False)["w"].to(dev)     # same weights on every rank
         slopes = torch.full((l.Cout,), synth.PRELU_SLOPE, device=dev) if l.prelu else None
         conv = nw.NestedConv2d(w, l.stride, l.pad, l.m_o, l.m_i, math, transposed=l.transposed, outer_taps=l.r_o,
-                               output_padding=l.output_padding, prelu_slopes=slopes, transform=False)
+                               output_padding=l.output_padding, prelu_slopes=slopes, transform=False,
+                               depthwise=l.depthwise)
         # filter transform once, on rank 0 only (timed separately); the other ranks receive U
         # through the one collective of the run: a broadcast over NCCL (NVLink / NVSwitch)
         if rank == 0:
@@ -534,10 +550,16 @@ def main():
         for name, path, lmath in legs:
             try:
                 tot = 0.0
+                flops_avail = 0
                 lay = []
                 for l, conv, x, y, pl in zip(layers_all, convs, xs, ys, per_layer):
+                    if lmath is not None and l.depthwise:
+                        lay.append({"layer": l.name, "unavailable": "plain bf16 is not built for depthwise layers"})
+                        continue
+                    flops_avail += l.direct_flops()
                     if lmath is not None:
                         conv = nw.NestedConv2d(conv.w, l.stride, l.pad, l.m_o, l.m_i, lmath, transposed=l.transposed,
+                                               depthwise=l.depthwise,
                                                outer_taps=l.r_o, output_padding=l.output_padding,
                                                prelu_slopes=conv.prelu_slopes)
                     conv.workspace(x.shape[0], x.shape[2], x.shape[3], path)
@@ -574,9 +596,10 @@ def main():
                     ent["roofline_frac"] = own["frac"]
                     lay.append(ent)
                     del conv
-                own_us = sum(e["roofline"].get("r3", e["roofline"]["r2_plan"])["bound_us"] for e in lay)
+                own_us = sum(e["roofline"].get("r3", e["roofline"]["r2_plan"])["bound_us"] for e in lay
+                             if "roofline" in e)
                 compare[name] = {"ms_per_step": round(tot, 4),
-                                 "tflops_direct_equiv": round(flops_rank / (tot / 1e3) / 1e12, 2),
+                                 "tflops_direct_equiv": round(flops_avail / (tot / 1e3) / 1e12, 2),
                                  "roofline_frac": round(own_us / (tot * 1e3), 4),
                                  "per_layer": lay}
                 if lmath is not None:
@@ -760,6 +783,8 @@ def reference_arm(args, layers, world, rank):
         for l, (x, w) in zip(layers, arrays):
             if l.transposed:
                 direct.conv_transpose2d(x, w, l.stride, l.pad, l.output_padding)
+            elif l.depthwise:
+                direct.conv2d_depthwise(x, w, l.stride, l.pad)
             else:
                 direct.conv2d(x, w, l.stride, l.pad)
 

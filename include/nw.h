@@ -39,7 +39,8 @@
  *    three hot kernels with programmatic dependent launch; NW_FUSED_C1=0 turns
  *    off the single-kernel path for one-input-channel layers; NW_CLUSTER=1
  *    disables the CTA pairs (B multicast) of the plain contraction; NW_INPUT_TMA=0 selects
- *    the first-round input transform instead of the persistent TMA-fed kernel; NW_GEMM_G=g
+ *    the first-round input transform instead of the persistent TMA-fed kernel (bf16 x);
+ *    NW_GEMM_G=g
  *    caps its 128-slice blocks per unit (default 16); NW_KBK=64 forces 64-wide
  *    K blocks for narrow layers (default: 16 / 32 when cin_pad is 16 / 32);
  *    NW_DEBUG_SYNC=1 synchronises after every launch and names a faulting kernel on stderr.
@@ -87,7 +88,10 @@ typedef enum {
   NW_ATTR_OUTPUT_PADDING = 3, /* transposed only; default 0 */
   NW_ATTR_OUTER_TAPS = 4,     /* r_o: 3 = paper's fixed 3x3 tile grid (default); 0 = mixed ceil(K'/3) (R8) */
   NW_ATTR_PAD = 5,            /* zero padding on every side; default K/2 */
-  NW_ATTR_PRELU = 6           /* 0/1: fuse y = y >= 0 ? y : slope[c]*y into the store (slopes via nw_plan_set_prelu) */
+  NW_ATTR_PRELU = 6,          /* 0/1: fuse y = y >= 0 ? y : slope[c]*y into the store (slopes via nw_plan_set_prelu) */
+  NW_ATTR_DEPTHWISE = 7       /* 0/1: depthwise layer (Cin == Cout == C, w [C][1][K][K], groups = C; Table I's
+                                 PNASNet row): no channel contraction, the transform-domain product
+                                 is per channel; stride 1; math FP32_SIMT or BF16X3 (default 0) */
 } nw_attr_t;
 
 /* Integer tables exported for bit-exact comparison with the CPU oracle
@@ -200,6 +204,18 @@ NW_API nw_status_t nw_conv_forward_host(nw_plan_t plan, const void *x_host, cons
 NW_API nw_status_t nw_profile_begin(void);
 NW_API nw_status_t nw_profile_end(const char **names, unsigned long long *launches, double *ms,
                                   size_t cap, size_t *n);
+
+/* Decomposition algorithm of section IV.B, host only: the expression tree
+ * of F(M, R; S) over one base kernel F(m, r) -- stride Winograd split (Eq. 2.7) while
+ * S > 1, nested Winograd (III.A) while R > r, output lengths matched with
+ * F(n.m, r) = n.F(m, r) -- written as its reverse-Polish token stream, NUL-terminated,
+ * into rpn[0..cap) (tokens K<m>,<r> NEST<d> REP<n> SUM<k>; Eq. 4.1 is
+ * "K2,2 NEST2 K2,2 REP2 SUM2"); *len receives the string length, *M the resolved output
+ * length per tile.  rpn may be NULL (size query).  Errors: NW_ERR_INVALID for arguments
+ * < 1 (or absurdly large) or cap too small; NW_ERR_UNSUPPORTED when nesting would need
+ * m < r (holes, R6).  The GPU kernels execute the two-level plans with r = 3
+ * taps and stride <= 2; deeper or stride-3 plans are planned, not executed. */
+NW_API nw_status_t nw_decompose(int R, int S, int m, int r, char *rpn, size_t cap, size_t *len, int *M);
 
 /* EWMM multiplications of one nested forward (slices * P * Cin_e * Cout_e). */
 NW_API nw_status_t nw_count_mults(nw_plan_t plan, int N, int H, int W, unsigned long long *ewmm);

@@ -119,6 +119,26 @@ def conv_transpose2d_at(x: np.ndarray, w: np.ndarray, stride: int, pad: int, poi
     return out
 
 
+def conv2d_depthwise(x: np.ndarray, w: np.ndarray, stride: int = 1, pad: int = 0) -> np.ndarray:
+    """Depthwise (groups = C) Eq. 2.1 in float64: channel c of y sees only channel c of x and
+    filter c -- y[n, c, i, j] = sum_{r, s} xpad[n, c, i*S + r, j*S + s] * w[c, 0, r, s]
+    (Table I's PNASNet depthwise row).  x [N, C, H, W], w [C, 1, K, K]."""
+    x = np.asarray(x, dtype=np.float64)
+    w = np.asarray(w, dtype=np.float64)
+    N, C, H, W = x.shape
+    C2, one, KH, KW = w.shape
+    assert C == C2 and one == 1
+    Ho, Wo = out_size(H, KH, stride, pad), out_size(W, KW, stride, pad)
+    xp = np.zeros((N, C, H + 2 * pad, W + 2 * pad))
+    xp[:, :, pad:pad + H, pad:pad + W] = x
+    y = np.zeros((N, C, Ho, Wo))
+    for r in range(KH):
+        for s in range(KW):
+            win = xp[:, :, r:r + stride * (Ho - 1) + 1:stride, s:s + stride * (Wo - 1) + 1:stride]
+            y += win * w[None, :, 0, r, s, None, None]
+    return y
+
+
 def conv2d_bruteforce(x, w, stride: int = 1, pad: int = 0):
     """Eq. 2.1 as seven nested scalar loops (tiny inputs only)."""
     N, C, H, W = len(x), len(x[0]), len(x[0][0]), len(x[0][0][0])

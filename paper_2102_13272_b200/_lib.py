@@ -18,7 +18,7 @@ NW_OK, NW_ERR_INVALID, NW_ERR_UNSUPPORTED, NW_ERR_NOMEM, NW_ERR_CUDA, NW_ERR_WOR
 MATH_FP32_SIMT, MATH_BF16X3, MATH_BF16 = 0, 1, 2
 DTYPE_F32, DTYPE_BF16 = 0, 1
 (ATTR_MATH, ATTR_DTYPE, ATTR_TRANSPOSED, ATTR_OUTPUT_PADDING, ATTR_OUTER_TAPS, ATTR_PAD,
- ATTR_PRELU) = range(7)
+ ATTR_PRELU, ATTR_DEPTHWISE) = range(8)
 (TABLE_BT, TABLE_G, TABLE_AT, TABLE_GATHER, TABLE_SCATTER, TABLE_ORIGINS, TABLE_PHASE_TAPS,
  TABLE_DIMS) = range(8)
 
@@ -27,7 +27,7 @@ EXPORTS = [
     "nw_plan_tables", "nw_output_size", "nw_workspace_size", "nw_workspace_size_ola",
     "nw_workspace_size_direct", "nw_transform_filter", "nw_conv_forward", "nw_conv_ola", "nw_conv_direct",
     "nw_count_mults", "nw_launch_count", "nw_status_str", "nw_workspace_size_host", "nw_conv_forward_host",
-    "nw_profile_begin", "nw_profile_end",
+    "nw_profile_begin", "nw_profile_end", "nw_decompose",
 ]
 
 
@@ -87,6 +87,7 @@ def load() -> ctypes.CDLL:
         "nw_profile_begin": (st, []),
         "nw_profile_end": (st, [ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_ulonglong),
                                 ctypes.POINTER(ctypes.c_double), SZ, ctypes.POINTER(SZ)]),
+        "nw_decompose": (st, [I, I, I, I, ctypes.c_char_p, SZ, ctypes.POINTER(SZ), ctypes.POINTER(I)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -128,7 +129,7 @@ class Plan:
     def __init__(self, K: int, stride: int, m_outer: int, m_inner: int, Cin: int, Cout: int, *,
                  math: int = MATH_BF16X3, dtype: int = DTYPE_F32, transposed: bool = False,
                  output_padding: int = 0, outer_taps: int = 3, pad: Optional[int] = None,
-                 prelu_slopes=None):
+                 prelu_slopes=None, depthwise: bool = False):
         lib = load()
         self._h = ctypes.c_void_p()
         _chk(lib.nw_plan(K, stride, m_outer, m_inner, Cin, Cout, ctypes.byref(self._h)), "nw_plan")
@@ -137,11 +138,13 @@ class Plan:
             _chk(lib.nw_plan_set(self._h, attr, val), f"nw_plan_set({attr})")
         if pad is not None:
             _chk(lib.nw_plan_set(self._h, ATTR_PAD, pad), "nw_plan_set(pad)")
+        if depthwise:
+            _chk(lib.nw_plan_set(self._h, ATTR_DEPTHWISE, 1), "nw_plan_set(depthwise)")
         self._slopes = prelu_slopes  # keep the device buffer alive
         if prelu_slopes is not None:
             _chk(lib.nw_plan_set_prelu(self._h, _ptr(prelu_slopes)), "nw_plan_set_prelu")
         _chk(lib.nw_plan_finalize(self._h), "nw_plan_finalize")
-        self.K, self.stride, self.Cin, self.Cout = K, stride, Cin, Cout
+        self.K, self.stride, self.Cin, self.Cout, self.depthwise = K, stride, Cin, Cout, depthwise
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -203,6 +206,16 @@ class Plan:
     def direct(self, x, w, y, N: int, H: int, W: int, ws, ws_bytes: int, stream=None) -> None:
         _chk(load().nw_conv_direct(self._h, _ptr(x), _ptr(w), _ptr(y), N, H, W, _ptr(ws), ws_bytes,
                                    _stream(stream)), "nw_conv_direct")
+
+
+def decompose(R: int, S: int, m: int, r: int):
+    """Section IV.B decomposition (host only): (reverse-Polish token string, output length M)."""
+    lib = load()
+    n, M = ctypes.c_size_t(), ctypes.c_int()
+    _chk(lib.nw_decompose(R, S, m, r, None, 0, ctypes.byref(n), ctypes.byref(M)), "nw_decompose")
+    buf = ctypes.create_string_buffer(n.value + 1)
+    _chk(lib.nw_decompose(R, S, m, r, buf, n.value + 1, ctypes.byref(n), ctypes.byref(M)), "nw_decompose")
+    return buf.value.decode(), M.value
 
 
 def launch_count() -> int:

@@ -53,9 +53,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
     """Compile the stale csrc/*.cu objects and link libnw.so; skipped when up to date."""
     os.makedirs(BUILD, exist_ok=True)
     hdr = os.path.join(os.path.dirname(HERE), "include", "nw.h")
-    newest = max(_deps_mtime(), os.path.getmtime(hdr), os.path.getmtime(__file__))
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
-        return LIB
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     hmt = max([os.path.getmtime(h) for h in headers] + [os.path.getmtime(hdr), os.path.getmtime(__file__)])
     srcs = sources()
@@ -63,6 +60,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=max(1, min(16, len(todo)))) as ex:
         list(ex.map(lambda s: _compile(s, verbose), todo))
     objs = [os.path.join(BUILD, s.replace(".cu", ".o")) for s in srcs]
+    # per-object staleness decides what compiles; the library relinks when any object is newer
+    if not todo and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
+        return LIB
     cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

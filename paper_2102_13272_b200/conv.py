@@ -22,21 +22,26 @@ class NestedConv2d:
     def __init__(self, w: torch.Tensor, stride: int = 1, pad: Optional[int] = None, m_outer: int = 3,
                  m_inner: int = 3, math: int = MATH_BF16X3, transposed: bool = False,
                  output_padding: int = 0, outer_taps: int = 3, prelu_slopes: Optional[torch.Tensor] = None,
-                 transform: bool = True):
+                 transform: bool = True, depthwise: bool = False):
         """transform=False allocates U without computing it: a multi-GPU run transforms the
-        filter on rank 0 only and broadcasts U (dist.broadcast_filter) into the other ranks'."""
+        filter on rank 0 only and broadcasts U (dist.broadcast_filter) into the other ranks'.
+        depthwise=True: w is [C][1][K][K] (groups = C, Table I's PNASNet row), Cin = Cout = C."""
         if not w.is_cuda:
             raise ValueError("w must be a CUDA tensor")
         if w.dtype not in _DT:
             raise ValueError(f"unsupported dtype {w.dtype}")
         K = w.shape[-1]
         Cin, Cout = (w.shape[0], w.shape[1]) if transposed else (w.shape[1], w.shape[0])
+        if depthwise:
+            if w.shape[1] != 1:
+                raise ValueError("depthwise filters are [C][1][K][K]")
+            Cin = Cout = w.shape[0]
         self.w = w.contiguous()
         self.dtype = w.dtype
         self.prelu_slopes = prelu_slopes
         self.plan = Plan(K, stride, m_outer, m_inner, Cin, Cout, math=math, dtype=_DT[w.dtype],
                          transposed=transposed, output_padding=output_padding, outer_taps=outer_taps,
-                         pad=pad, prelu_slopes=prelu_slopes)
+                         pad=pad, prelu_slopes=prelu_slopes, depthwise=depthwise)
         self.info = self.plan.info()
         self.Cin, self.Cout = Cin, Cout
         self.U = torch.empty(self.info["filter_bytes"], dtype=torch.uint8, device=w.device)

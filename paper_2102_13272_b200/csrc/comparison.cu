@@ -170,7 +170,9 @@ nw_status_t run_comparison(nw_plan_t p, const void* x, const void* w, void* y, i
   if ((st = launch_filter_transform(p, g, w, U, s)) != NW_OK) return st;
   st = (path == kPathDirect) ? launch_pack_input(p, g, x, V, s) : launch_input_transform(p, g, x, V, s);
   if (st != NW_OK) return st;
-  if (p->math == NW_MATH_FP32_SIMT)
+  if (p->depthwise)  // per-channel sum over the shifted blocks / taps (no channel contraction)
+    st = launch_depthwise_product(p, g, V, static_cast<const float*>(U), M, s);
+  else if (p->math == NW_MATH_FP32_SIMT)
     st = launch_gemm_simt(p, g, static_cast<const float*>(V), static_cast<const float*>(U), M, s);
   else
     st = launch_gemm_tc(p, g, V, U, M, s);

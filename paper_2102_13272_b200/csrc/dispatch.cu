@@ -49,7 +49,7 @@ bool fused_c1_eligible(const nw_plan_st* p, const Geometry& g) {
     const char* v = getenv("NW_FUSED_C1");
     return v ? atoi(v) : 1;
   }();
-  return on && g.path == kPathNested && g.mode == 0 && g.cin_e == 1 && g.mi == 3 && g.nph == 1 && g.mo >= 2 &&
+  return on && !p->depthwise && g.path == kPathNested && g.mode == 0 && g.cin_e == 1 && g.mi == 3 && g.nph == 1 && g.mo >= 2 &&
          g.Pa <= 30;  // V of 32 slices in shared memory: up to F(4,3) / F(5,2) (x) F(3,3)
 }
 

@@ -87,7 +87,14 @@ __global__ void __launch_bounds__(128) filter_transform_kernel(const WT* __restr
   }
 }
 
-nw_status_t launch_filter_transform(const nw_plan_st* p, const Geometry& g, const void* w, void* U, cudaStream_t s) {
+nw_status_t launch_filter_transform(const nw_plan_st* p, const Geometry& g_in, const void* w, void* U,
+                                    cudaStream_t s) {
+  Geometry g = g_in;
+  if (p->depthwise) {  // w [C][1][K][K]: one single-input-channel filter per channel -> U [P][cout_pad][nsh]
+    g.Cin = 1;
+    g.cin_e = 1;
+    g.cin_pad = 1;
+  }
   GhatParam G{};
   const NestedAxis ax = path_axis(p, g.path);
   G.Pa = ax.Pa;
@@ -96,7 +103,7 @@ nw_status_t launch_filter_transform(const nw_plan_st* p, const Geometry& g, cons
     for (int k = 0; k < G.R; ++k) G.g[q * G.R + k] = (g.path == kPathDirect) ? 1.0 : rdouble(g_hat(ax, q, k));
   const long long n = (long long)g.cout_pad * g.nsh * g.cin_pad;
   const int blocks = (int)((n + 127) / 128);
-  const bool bf = p->math != NW_MATH_FP32_SIMT;
+  const bool bf = p->math != NW_MATH_FP32_SIMT && !p->depthwise;  // depthwise U stays fp32
   LaunchScope scope_("filter_transform", s);
   if (p->dtype == NW_DTYPE_BF16) {
     const __nv_bfloat16* wb = static_cast<const __nv_bfloat16*>(w);

@@ -56,7 +56,7 @@ struct nw_plan_st {
   int K, stride, m_o, m_i, Cin, Cout;
   int math = NW_MATH_BF16X3;
   int dtype = NW_DTYPE_F32;
-  int transposed = 0, output_padding = 0, outer_taps = 3, pad = -1, prelu = 0;
+  int transposed = 0, output_padding = 0, outer_taps = 3, pad = -1, prelu = 0, depthwise = 0;
   const float *slopes = nullptr;
   bool finalized = false;
   // derived at finalize
@@ -113,6 +113,9 @@ nw_status_t launch_output_transform_pre(const nw_plan_st *p, const Geometry &g, 
                                         cudaStream_t s);
 nw_status_t launch_gemm_tc(const nw_plan_st *p, const Geometry &g, const void *V, const void *U,
                            float *M, cudaStream_t s);
+// depthwise layers: per-channel transform-domain product (depthwise.cu)
+nw_status_t launch_depthwise_product(const nw_plan_st *p, const Geometry &g, const void *V, const float *U, float *M,
+                                     cudaStream_t s);
 // single-input-channel layers: the whole nested pipeline in one kernel (fused_small.cuh)
 bool fused_c1_eligible(const nw_plan_st *p, const Geometry &g);
 nw_status_t launch_fused_c1(const nw_plan_st *p, const Geometry &g, const void *x, const void *U, void *y,

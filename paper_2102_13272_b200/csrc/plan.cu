@@ -82,6 +82,10 @@ nw_status_t finalize(nw_plan_st *p) {
   if (p->finalized) return NW_OK;
   if (p->pad < 0) p->pad = p->K / 2;
   if (p->transposed && p->stride != 2) return NW_ERR_UNSUPPORTED;
+  if (p->depthwise) {  // groups = C: one filter per channel, no channel sum
+    if (p->Cin != p->Cout) return NW_ERR_INVALID;
+    if (p->stride != 1 || p->transposed || p->math == NW_MATH_BF16) return NW_ERR_UNSUPPORTED;
+  }
   int mode, n_sp, Kp, off[2], taps[2][kMaxTaps];
   phase_split(p, &mode, &n_sp, &Kp, off, taps);
   p->Kp = Kp;
@@ -186,6 +190,7 @@ size_t u_bytes(const Geometry &g) {
 }
 size_t filter_bytes(const nw_plan_st *p) {
   const long long P = (long long)p->ax.Pa * p->ax.Pa;
+  if (p->depthwise) return (size_t)(P * p->cout_pad * 4);  // fp32 U [P][cout_pad]: one filter per channel
   return (size_t)(P * p->cout_pad * p->cin_pad * 4);  // fp32 or bf16 hi + lo planes
 }
 
@@ -250,6 +255,9 @@ nw_status_t nw_plan_set(nw_plan_t p, nw_attr_t attr, long long v) {
     case NW_ATTR_PRELU:
       if (v != 0 && v != 1) return NW_ERR_INVALID;
       p->prelu = (int)v; return NW_OK;
+    case NW_ATTR_DEPTHWISE:
+      if (v != 0 && v != 1) return NW_ERR_INVALID;
+      p->depthwise = (int)v; return NW_OK;
   }
   return NW_ERR_INVALID;
 }
@@ -392,7 +400,9 @@ nw_status_t nw_count_mults(nw_plan_t p, int N, int H, int W, unsigned long long 
   nw_status_t st = finalize(p);
   if (st != NW_OK) return st;
   Geometry g = make_geometry(p, N, H, W);
-  *ewmm = (unsigned long long)g.T * g.P * g.cin_e * g.cout_e;
+  // depthwise: one product per (slice, point, channel) -- no channel contraction
+  *ewmm = (unsigned long long)g.T * g.P * (p->depthwise ? (unsigned long long)g.cout_e
+                                                         : (unsigned long long)g.cin_e * g.cout_e);
   return NW_OK;
 }
 

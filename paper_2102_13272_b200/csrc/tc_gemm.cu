@@ -647,7 +647,8 @@ bool gemm_fused_eligible(const nw_plan_st* p, const Geometry& g) {
     const char* v = getenv("NW_FUSE_AI");
     return v ? atoi(v) : 1;
   }();
-  return on && g.path == kPathNested && p->math != NW_MATH_FP32_SIMT && (g.cout_pad == 32 || g.cout_pad == 64) &&
+  return on && !p->depthwise && g.path == kPathNested && p->math != NW_MATH_FP32_SIMT &&
+         (g.cout_pad == 32 || g.cout_pad == 64) &&
          g.mi == 3 && g.nsh == 1;
 }
 

@@ -38,6 +38,7 @@ class Layer:
     wdist: str = "he"           # he | unif11
     seed: int = 0
     prelu: bool = False
+    depthwise: bool = False     # groups = Cin = Cout: w [C][1][K][K] (Table I's PNASNet row)
 
     @property
     def Ho(self) -> int:
@@ -53,6 +54,8 @@ class Layer:
 
     def direct_flops(self) -> int:
         """2 * MACs of the native convolution (Eq. 2.1; GOPs convention of P:164)."""
+        if self.depthwise:
+            return 2 * self.N * self.Ho * self.Wo * self.Cout * self.K * self.K
         if self.transposed:
             return 2 * self.N * self.H * self.W * self.Cin * self.Cout * self.K * self.K
         return 2 * self.N * self.Ho * self.Wo * self.Cin * self.Cout * self.K * self.K
@@ -88,14 +91,17 @@ CONFIGS: Dict[str, Layer] = {
 # Table I of the paper (ZCU102): the conv2d layer shapes (Cout, Cin, H, W), measured
 # there as nested vs OLA-Winograd GOPs.  Weights / images of SRCNN are not available: the
 # synthetic stand-ins use BASELINE configs[1]'s distributions; batch 8 (the paper runs one image).
-# The depthwise PNASNet 7x7 row needs a depthwise path, which is not built.
+# The depthwise PNASNet 7x7 row ((54, 54, 83, 83)) runs the depthwise path (groups = 54,
+# same padding; the paper gives no padding: 3 keeps 83 x 83), He-normal over the 49 taps.
 CONFIGS.update({
     "t1_srcnn9": Layer("t1_srcnn9", 8, 1, 64, 256, 256, 9, 1, 4, m_o=4, seed=61),
+    "t1_pnas_dw7": Layer("t1_pnas_dw7", 8, 54, 54, 83, 83, 7, 1, 3, m_o=4, seed=64, depthwise=True),
     "t1_srcnn5a": Layer("t1_srcnn5a", 8, 64, 32, 256, 256, 5, 1, 2, m_o=4, r_o=0, seed=62),
     "t1_srcnn5b": Layer("t1_srcnn5b", 8, 32, 1, 256, 256, 5, 1, 2, m_o=4, r_o=0, seed=63),
 })
-TABLE1 = ["t1_srcnn9", "t1_srcnn5a", "t1_srcnn5b"]
-TABLE1_PAPER_SPEEDUP = {"t1_srcnn9": 3.29, "t1_srcnn5a": 1.43, "t1_srcnn5b": 1.43}
+TABLE1 = ["t1_srcnn9", "t1_pnas_dw7", "t1_srcnn5a", "t1_srcnn5b"]
+TABLE1_PAPER_SPEEDUP = {"t1_srcnn9": 3.29, "t1_pnas_dw7": 1.41, "t1_srcnn5a": 1.43,
+                        "t1_srcnn5b": 1.43}
 
 C2_SWEEP = ["c2k5", "c2k7", "c2k9"]
 C5_NET = ["c5_conv1", "c5_conv2", "c5_conv3", "c5_conv4", "c5_deconv"]
@@ -132,6 +138,9 @@ def make_inputs(layer: Layer, x: bool = True) -> Dict[str, torch.Tensor]:
         # keep the draw order (x first, then w) even when x is not materialised
         gen = torch.Generator().manual_seed(layer.seed)
         _draw(gen, (layer.N, layer.Cin, layer.H, layer.W), layer.xdist, 1)
+    if layer.depthwise:   # one K x K filter per channel: fan-in K^2
+        out["w"] = _draw(gen, (layer.Cout, 1, layer.K, layer.K), layer.wdist, layer.K * layer.K).to(dt)
+        return out
     wshape = ((layer.Cin, layer.Cout, layer.K, layer.K) if layer.transposed
               else (layer.Cout, layer.Cin, layer.K, layer.K))
     out["w"] = _draw(gen, wshape, layer.wdist, layer.Cin * layer.K * layer.K).to(dt)

@@ -19,7 +19,7 @@ from paper_2102_13272_b200 import MATH_BF16X3, MATH_FP32_SIMT, NestedConv2d  # n
 spec = json.loads(sys.argv[1])
 base = synth.CONFIGS[spec.pop("config")]
 math = {"bf16x3": MATH_BF16X3, "fp32": MATH_FP32_SIMT}[spec.pop("math", "bf16x3")]
-extra = {k: spec.pop(k) for k in ("m_o", "r_o") if k in spec}
+extra = {k: spec.pop(k) for k in ("m_o", "r_o", "dtype", "xdist") if k in spec}
 layer = synth.small(base, **spec) if spec else base
 if extra:
     layer = layer.with_(**extra)

@@ -161,3 +161,38 @@ def test_forward_argument_errors_without_touching_memory():
     # comparison paths validate the same way
     assert lib.nw_conv_ola(p.handle, FAKE, FAKE, FAKE, 0, 20, 20, FAKE, 1 << 30, None) == _lib.NW_ERR_INVALID
     assert lib.nw_conv_direct(p.handle, FAKE, FAKE, FAKE, 2, 20, 20, FAKE, 16, None) == _lib.NW_ERR_WORKSPACE
+
+
+def test_decompose_matches_oracle_planner():
+    # the library's section IV.B planner (csrc/decompose.cu) vs the oracle's (oracle/planner.py):
+    # same token stream and output length over the Fig. 7 kernels, strides 1-3 and R up to 30
+    from oracle import planner
+    kernels = [(2, 2), (3, 3), (4, 4), (6, 3), (4, 3), (3, 2), (5, 3), (4, 2)]
+    for (m, r) in kernels:
+        for S in (1, 2, 3):
+            for R in list(range(1, 19)) + [25, 27, 30]:
+                p = planner.plan(R, S, m, r)
+                assert _lib.decompose(R, S, m, r) == (planner.rpn_text(p), p.M), (R, S, m, r)
+
+
+def test_decompose_errors():
+    import pytest
+    with pytest.raises(_lib.NWError):
+        _lib.decompose(0, 1, 3, 3)
+    with pytest.raises(_lib.NWError):
+        _lib.decompose(5, 1, 2, 3)      # m < r nesting leaves holes
+    assert _lib.decompose(3, 1, 2, 3) == ("K2,3", 2)   # no nesting needed: fine
+
+
+def test_depthwise_plan_info_and_errors():
+    # depthwise (Table I PNASNet row): U holds one fp32 filter per channel; EWMM count has no
+    # channel product; Cin != Cout and stride 2 are refused
+    p = _lib.Plan(7, 1, 4, 3, 54, 54, depthwise=True)
+    inf = p.info()
+    assert inf["filter_bytes"] == 900 * 64 * 4 and inf["single_kernel"] == 0 and inf["m_rows"] == 900
+    assert p.count_mults(8, 83, 83) == 8 * 7 * 7 * 900 * 54
+    import pytest
+    with pytest.raises(_lib.NWError):
+        _lib.Plan(7, 1, 4, 3, 54, 32, depthwise=True)
+    with pytest.raises(_lib.NWError):
+        _lib.Plan(7, 2, 4, 3, 54, 54, depthwise=True)

@@ -54,18 +54,19 @@ BITWISE = [
     (C4B, {"NW_KBK": "64"}),
     (C4B, {"NW_PIPE_CHUNKS": "2"}),
     (C3, {"NW_PIPE_CHUNKS": "2", "NW_GEMM_CTAS": "1"}),   # grid cap below a CTA pair: unpaired launch
-    # persistent TMA-fed input transform vs the first-round kernel: same fp32 operation sequence.
-    # The TMA path needs 16-byte x rows (W % 4 == 0 fp32, W % 8 == 0 bf16); window starts at
-    # every 16-byte phase (pad 2 / 4, advance 9 / 12) and several tasks per CTA (in-loop refill)
-    ({**C2, "W": 52}, {"NW_INPUT_TMA": "0"}),
-    ({**C2, "N": 9, "H": 64, "W": 64}, {"NW_INPUT_TMA": "0"}),                    # 576 tasks
-    ({**C2, "config": "c2k5", "W": 52}, {"NW_INPUT_TMA": "0"}),   # F(4,2) (x) F(3,3): L = 17, P_a = 25, pad 2
-    ({**C2, "config": "c2k7", "N": 5, "H": 61, "W": 60}, {"NW_INPUT_TMA": "0"}),  # pad 3
-    ({**C3, "W": 40}, {"NW_INPUT_TMA": "0"}),                    # bf16 x, 256 channels
-    ({**C3, "N": 6, "H": 64, "W": 64}, {"NW_INPUT_TMA": "0"}),   # bf16, 6 x 6 x 3 x 16 tasks
-    ({"config": "c5_deconv", "N": 2, "H": 23, "W": 36}, {"NW_INPUT_TMA": "0"}),   # transposed input side
-    ({"config": "c2k9", "N": 2, "H": 40, "W": 36, "Cin": 32, "Cout": 64, "m_o": 3}, {"NW_INPUT_TMA": "0"}),
-    ({"config": "c2k9", "N": 3, "H": 50, "W": 44, "Cin": 64, "Cout": 32, "m_o": 3}, {"NW_INPUT_TMA": "0"}),
+    # persistent TMA-fed input transform (bf16 x) vs the first-round kernel: same fp32 operation
+    # sequence.  The TMA path needs 16-byte x rows (W % 8 == 0 for bf16); window starts at every
+    # 16-byte phase (pad 2 / 3 / 4, advance 9 / 12) and several tasks per CTA (in-loop refill)
+    ({**C3, "W": 40}, {"NW_INPUT_TMA": "0"}),                    # 256 channels
+    ({**C3, "N": 6, "H": 64, "W": 64}, {"NW_INPUT_TMA": "0"}),   # 6 x 6 x 3 x 16 tasks
+    ({**C2, "W": 56, "dtype": "bf16"}, {"NW_INPUT_TMA": "0"}),
+    ({**C2, "N": 9, "H": 64, "W": 64, "dtype": "bf16"}, {"NW_INPUT_TMA": "0"}),   # 576 tasks
+    ({**C2, "config": "c2k5", "W": 56, "dtype": "bf16"}, {"NW_INPUT_TMA": "0"}),  # F(4,2)(x)F(3,3), pad 2
+    ({**C2, "config": "c2k7", "N": 5, "H": 61, "W": 64, "dtype": "bf16"}, {"NW_INPUT_TMA": "0"}),  # pad 3
+    ({"config": "c2k9", "N": 2, "H": 40, "W": 40, "Cin": 32, "Cout": 64, "m_o": 3, "dtype": "bf16"},
+     {"NW_INPUT_TMA": "0"}),
+    ({"config": "c2k9", "N": 3, "H": 50, "W": 48, "Cin": 64, "Cout": 32, "m_o": 3, "dtype": "bf16"},
+     {"NW_INPUT_TMA": "0"}),
 ]
 
 
@@ -88,7 +89,7 @@ ARITH = [
 def test_arithmetic_tunables_meet_gate(spec, env, tmp_path):
     y = _run(dict(spec), env, tmp=tmp_path)
     s = dict(spec)
-    extra = {k: s.pop(k) for k in ("m_o", "r_o") if k in s}
+    extra = {k: s.pop(k) for k in ("m_o", "r_o", "dtype", "xdist") if k in s}
     layer = synth.small(synth.CONFIGS[s.pop("config")], **s).with_(**extra)
     check_parity(y, _ref(layer, synth.make_inputs(layer)), "bf16x3", layer.dtype)
 

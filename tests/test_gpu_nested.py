@@ -217,16 +217,16 @@ def test_output_buffer_is_validated():
     assert conv(x, y) is y
 
 
-# the persistent TMA-fed input transform (input_transform_tma.cuh) runs where x rows are
-# 16-byte multiples; these shapes take it, with more tasks than two per CTA (in-loop TMA
+# the persistent TMA-fed input transform (input_transform_tma.cuh) runs for bf16 x whose rows
+# are 16-byte multiples; these shapes take it, with more tasks than CTA slots (in-loop TMA
 # refills), every 16-byte phase of the window start and ragged tile edges
 TMA_SHAPES = {
-    "c2k9": synth.small(synth.CONFIGS["c2k9"], N=8, H=61, W=64),
-    "c2k5": synth.small(synth.CONFIGS["c2k5"], N=4, H=50, W=76),
-    "c2k7": synth.small(synth.CONFIGS["c2k7"], N=3, H=47, W=92),
+    "c2k9": synth.small(synth.CONFIGS["c2k9"], N=8, H=61, W=64).with_(dtype="bf16"),
+    "c2k5": synth.small(synth.CONFIGS["c2k5"], N=4, H=50, W=72).with_(dtype="bf16"),
+    "c2k7": synth.small(synth.CONFIGS["c2k7"], N=3, H=47, W=88).with_(dtype="bf16"),
     "c3": synth.small(synth.CONFIGS["c3"], N=3, H=40, W=48, Cin=64, Cout=64),
-    "c5_deconv": synth.small(synth.CONFIGS["c5_deconv"], N=2, H=30, W=44),
-    "c2k9_m3": synth.small(synth.CONFIGS["c2k9"], N=4, H=45, W=60).with_(m_o=3),
+    "c5_deconv": synth.small(synth.CONFIGS["c5_deconv"], N=2, H=30, W=40).with_(dtype="bf16"),
+    "c2k9_m3": synth.small(synth.CONFIGS["c2k9"], N=4, H=45, W=64).with_(m_o=3, dtype="bf16"),
 }
 
 

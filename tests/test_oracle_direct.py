@@ -70,3 +70,19 @@ def test_transposed_output_size_fsrcnn():
     # DESIGN.md#R11: 9x9 stride 2, pad 4, output_padding 1 maps 540x960 -> 1080x1920
     H, W, K = 540, 960, 9
     assert (H - 1) * 2 - 8 + K + 1 == 1080 and (W - 1) * 2 - 8 + K + 1 == 1920
+
+
+@pytest.mark.parametrize("K,pad,stride", [(7, 3, 1), (3, 1, 1), (5, 0, 2)])
+def test_depthwise_vs_torch_groups_and_bruteforce(K, pad, stride):
+    # Table I's depthwise row: groups = C -- an independent library (torch fp64
+    # groups=C) and the per-channel brute force of Eq. 2.1
+    rng = np.random.default_rng(K)
+    x = rng.standard_normal((2, 5, 11, 9))
+    w = rng.standard_normal((5, 1, K, K))
+    y = direct.conv2d_depthwise(x, w, stride, pad)
+    ref = torch.nn.functional.conv2d(torch.from_numpy(x), torch.from_numpy(w), stride=stride, padding=pad,
+                                     groups=5).numpy()
+    np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-12)
+    for c in range(5):
+        bf = direct.conv2d_bruteforce(x[:, c:c + 1].tolist(), w[c:c + 1].tolist(), stride, pad)
+        np.testing.assert_allclose(y[:, c:c + 1], np.array(bf), rtol=1e-12, atol=1e-12)
