@@ -39,7 +39,8 @@
  *    three hot kernels with programmatic dependent launch; NW_FUSED_C1=0 turns
  *    off the single-kernel path for one-input-channel layers; NW_CLUSTER=1
  *    disables the CTA pairs (B multicast) of the plain contraction; NW_INPUT_TMA=0 selects
- *    the first-round input transform instead of the persistent TMA-fed kernel (bf16 x);
+ *    the first-round input transform instead of the persistent TMA-fed kernel (bf16 x;
+ *    NW_ITMA_F32=1 also fp32 x, NW_ITMA_CC=32 32 channels per task);
  *    NW_GEMM_G=g
  *    caps its 128-slice blocks per unit (default 16); NW_KBK=64 forces 64-wide
  *    K blocks for narrow layers (default: 16 / 32 when cin_pad is 16 / 32);

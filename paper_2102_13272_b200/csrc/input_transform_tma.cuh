@@ -1,15 +1,15 @@
 // input_transform_tma.cuh -- G2 on sm_100a: nested input transform V = B^T_hat X B_hat
 // as a persistent kernel fed by TMA halo-tile loads.
 //
-// Two CTAs per SM walk tasks (image n, tile row a_h, TW = 2 adjacent tiles along w, CC = 16
-// source channels), channel group fastest so the four CTAs filling one 128-byte V row run
-// side by side.  Per task:
+// Persistent CTAs walk tasks (image n, tile row a_h, TW = 2 adjacent tiles along w, CC = 32
+// source channels -- 16 warps, one CTA per SM; CC = 16: 8 warps, two CTAs per SM), channel
+// group fastest so the CTAs filling one 128-byte V row run side by side.  Per task:
 //   TMA     one 3-D box {window columns (+ up to 15 bytes so it starts 16-byte aligned),
 //           L rows, 16 channels} of x [N*Cin][H][W] lands in the CTA's window buffer;
 //           coordinates outside the image are zero-filled by the copy engine (= the
 //           convolution's zero padding), so there are no bounds tests.  The next task's box is
 //           issued as soon as pass 1 has read the buffer, so it lands during pass 2 (and while
-//           the SM's other CTA computes).
+//           an SM's other CTA computes).
 //   pass 1  thread = (channel, window column): B^T_hat along h (both levels, factored 1-D
 //           kernels of transforms.cuh) -> Hs[p_h][channel][column], fp32.
 //   pass 2  lane = (channel pair, (p_h, tile) combo): the L-long row of Hs along w -> P_a
@@ -30,10 +30,12 @@
 
 namespace nw {
 
-template <int MO, int RO, int MI, typename XT>
+template <int MO, int RO, int MI, typename XT, int CC_>
 struct ItCfg {
   using X = Ax<MO, RO, MI>;
-  static constexpr int CC = 16;                         // source channels per task
+  static constexpr int CC = CC_;                        // source channels per task (16 or 32)
+  static constexpr int NPR = CC / 2;                    // channel pairs: lanes per combo in pass 2
+  static constexpr int SUBS = 32 / NPR;                 // combos per warp pass
   static constexpr int TW = 2;                          // tiles per task along w
   static constexpr int ES = (int)sizeof(XT);
   static constexpr int WC = (TW - 1) * X::ADV + X::L;   // window columns used
@@ -48,20 +50,21 @@ struct ItCfg {
   static constexpr int HSTR = WC | 1;                   // odd row pitch of Hs (bank spread)
   static constexpr int HS = PA * CC * HSTR;             // floats
   static constexpr int COMBOS = PA * TW;                // (p_h, tile) rows of pass 2
-  static constexpr int GROUPS = (COMBOS + 3) / 4;       // 4 combos x 8 channel pairs per warp pass
-  static constexpr int WARPS = 8;
+  static constexpr int GROUPS = (COMBOS + SUBS - 1) / SUBS;  // SUBS combos x NPR pairs per warp pass
+  // 16 channels: 8 warps, two CTAs per SM; 32 channels: 16 warps, one CTA per SM (shared memory)
+  static constexpr int WARPS = CC == 16 ? 8 : 16;
   static constexpr int THREADS = WARPS * 32;
-  static constexpr int MINB = 2;                        // two CTAs per SM (<= 128 registers)
+  static constexpr int MINB = CC == 16 ? 2 : 1;         // <= 128 registers either way
   static constexpr size_t SMEM = (size_t)STAGE + (size_t)HS * 4 + 64;
   static_assert(BW <= 256 && L <= 256, "TMA box");
 };
 
-template <int MO, int RO, int MI, typename XT, int CINP>
-__global__ void __launch_bounds__(ItCfg<MO, RO, MI, XT>::THREADS, ItCfg<MO, RO, MI, XT>::MINB)
+template <int MO, int RO, int MI, typename XT, int CINP, int CC_>
+__global__ void __launch_bounds__(ItCfg<MO, RO, MI, XT, CC_>::THREADS, ItCfg<MO, RO, MI, XT, CC_>::MINB)
     input_transform_tma_kernel(const __grid_constant__ CUtensorMap mapX, void* __restrict__ Vout, Geometry g,
                                int cgroups, int wgroups, int ntasks) {
   using X = Ax<MO, RO, MI>;
-  using C = ItCfg<MO, RO, MI, XT>;
+  using C = ItCfg<MO, RO, MI, XT, CC_>;
   constexpr int PA = X::PA, L = X::L, CC = C::CC;
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* stage = smem;                                   // window (one buffer)
@@ -130,10 +133,10 @@ __global__ void __launch_bounds__(ItCfg<MO, RO, MI, XT>::THREADS, ItCfg<MO, RO, 
     }
 
     // ---------------- pass 2: rows along w, split, store V ----------------
-    const int pair = lane & 7, sub = lane >> 3;
+    const int pair = lane % C::NPR, sub = lane / C::NPR;
 #pragma unroll 1
     for (int grp = warp; grp < C::GROUPS; grp += C::WARPS) {
-      const int q = grp * 4 + sub;                  // (p_h, tile) combo of this lane
+      const int q = grp * C::SUBS + sub;            // (p_h, tile) combo of this lane
       const int ph = q / C::TW, tile = q % C::TW;
       const bool live = q < C::COMBOS && aw0 + tile < g.tiles_w;
       if (live) {
@@ -173,11 +176,21 @@ inline bool input_tma_enabled() {
   return on != 0;
 }
 
-template <int MO, int RO, int MI, typename XT, int CINP>
-static nw_status_t input_tma_launch(const Geometry& g, const void* x, void* V, cudaStream_t s) {
-  using C = ItCfg<MO, RO, MI, XT>;
-  auto kern = input_transform_tma_kernel<MO, RO, MI, XT, CINP>;
-  if (ensure_smem<input_transform_tma_kernel<MO, RO, MI, XT, CINP>>((int)C::SMEM) != NW_OK) return NW_ERR_CUDA;
+// NW_ITMA_CC=16|32: source channels per task (default 32: C3 0.432 ms against 0.485 with 16,
+// 0.565 with the first-round kernel; profiles/r2_input_transform.md)
+inline int input_tma_cc() {
+  static const int cc = [] {
+    const char* v = getenv("NW_ITMA_CC");
+    return v ? atoi(v) : 32;
+  }();
+  return cc;
+}
+
+template <int MO, int RO, int MI, typename XT, int CINP, int CC_>
+static nw_status_t input_tma_launch_cc(const Geometry& g, const void* x, void* V, cudaStream_t s) {
+  using C = ItCfg<MO, RO, MI, XT, CC_>;
+  auto kern = input_transform_tma_kernel<MO, RO, MI, XT, CINP, CC_>;
+  if (ensure_smem<input_transform_tma_kernel<MO, RO, MI, XT, CINP, CC_>>((int)C::SMEM) != NW_OK) return NW_ERR_CUDA;
   const uint64_t dims[3] = {(uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N * g.Cin};
   const uint64_t strides[2] = {(uint64_t)g.W * C::ES, (uint64_t)g.H * g.W * C::ES};
   const uint32_t box[3] = {(uint32_t)C::BW, (uint32_t)C::L, (uint32_t)C::CC};
@@ -199,16 +212,27 @@ static nw_status_t input_tma_launch(const Geometry& g, const void* x, void* V, c
   return check_launch();
 }
 
+template <int MO, int RO, int MI, typename XT, int CINP>
+static nw_status_t input_tma_launch(const Geometry& g, const void* x, void* V, cudaStream_t s) {
+  if (input_tma_cc() == 32 && g.Cin % 32 == 0 && ItCfg<MO, RO, MI, XT, 32>::SMEM <= 227 * 1024)
+    return input_tma_launch_cc<MO, RO, MI, XT, CINP, 32>(g, x, V, s);
+  return input_tma_launch_cc<MO, RO, MI, XT, CINP, 16>(g, x, V, s);
+}
+
 // The TMA kernel covers stride-1 inputs (incl. the transposed plan's input side) without
 // coverage phases, bf16x3 blocked V, every source channel real (Cin = cin_pad, a multiple of
 // 16) and 16-byte x row pitches (TMA).
 template <int MO, int RO, int MI, typename XT>
 inline bool input_tma_eligible(const Geometry& g) {
-  using C = ItCfg<MO, RO, MI, XT>;
-  // bf16 x only: with fp32 x (C2) the first-round kernel (32 channels per CTA, 64-byte V
-  // row segments) measured faster, 0.197 vs 0.245 ms per C2 layer; with bf16 x (C3) this
-  // kernel is faster, 0.484 vs 0.565 ms (profiles/r2_input_transform.md)
-  return input_tma_enabled() && sizeof(XT) == 2 && g.SR == 1 && g.nph == 1 && g.vblk && g.Cin == g.cin_pad && g.Cin % C::CC == 0 &&
+  using C = ItCfg<MO, RO, MI, XT, 16>;
+  // bf16 x only: with fp32 x (C2) the first-round kernel measured as fast or faster (0.197 ms per
+  // C2 layer against 0.203 with 32 channels per task, 0.243 with 16); with bf16 x (C3) this kernel
+  // is faster, 0.432 against 0.565 ms (profiles/r2_input_transform.md)
+  static const bool fp32_too = [] {  // NW_ITMA_F32=1: also fp32 x (measurement switch)
+    const char* v = getenv("NW_ITMA_F32");
+    return v && atoi(v) == 1;
+  }();
+  return input_tma_enabled() && (sizeof(XT) == 2 || fp32_too) && g.SR == 1 && g.nph == 1 && g.vblk && g.Cin == g.cin_pad && g.Cin % C::CC == 0 &&
          ((long long)g.W * C::ES) % 16 == 0 && 2 * C::SMEM <= 227 * 1024 && g.H < (1 << 30);
 }
 
