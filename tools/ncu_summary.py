@@ -46,7 +46,8 @@ KEYS = [
 STALLS = re.compile(r"^smsp__average_warps_issue_stalled_(\w+)_per_issue_active\.ratio$")
 KIND = {"input_transform": "input_transform", "contraction": "contraction_tc",
         "output_transform": "output_transform", "gemm_simt": "contraction_fp32_simt",
-        "filter_transform": "filter_transform", "ola": "ola", "direct": "direct", "fused_c1": "fused_c1"}
+        "filter_transform": "filter_transform", "ola": "ola", "direct": "direct", "fused_c1": "fused_c1",
+        "depthwise_product": "depthwise_product"}
 
 
 def short(name: str) -> str:
@@ -74,7 +75,10 @@ def launches(path: str, tag: str) -> str:
 
 
 def rep_metrics(path: str):
-    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):   # raw page exported on the GPU box (ncu -i rep --page raw --csv)
+        txt = open(path).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(txt.splitlines()))
     h, units = rows[0], rows[1]
     out = []
@@ -132,7 +136,12 @@ def main():
             md.append("")
             if "dram__bytes_read.sum" in d and "dram__bytes_write.sum" in d:
                 b = to_bytes(*d["dram__bytes_read.sum"]) + to_bytes(*d["dram__bytes_write.sum"])
-                layer = os.path.basename(rep).split("_")[2] if os.path.basename(rep).count("_") >= 3 else "?"
+                base = os.path.basename(rep).split(".")[0]          # prof_<tag>_<layer>_<kernel>
+                rest = base[len(f"prof_{a.tag}_"):] if base.startswith(f"prof_{a.tag}_") else base
+                layer = "?"
+                for kk in ("_input_transform", "_output_transform", "_contraction", "_depthwise", "_fused_c1"):
+                    if rest.endswith(kk):
+                        layer = rest[: -len(kk)]
                 for key, kind in KIND.items():
                     if key in d["kernel"]:
                         traffic[f"{kind}:{a.math}:{layer}:m{a.m_outer}"] = int(b)

@@ -34,7 +34,7 @@ def main():
     w, x = t["w"].cuda(), t["x"].cuda()
     slopes = torch.full((l.Cout,), synth.PRELU_SLOPE, device="cuda") if l.prelu else None
     conv = nw.NestedConv2d(w, l.stride, l.pad, l.m_o, l.m_i, math, transposed=l.transposed, outer_taps=l.r_o,
-                           output_padding=l.output_padding, prelu_slopes=slopes)
+                           output_padding=l.output_padding, prelu_slopes=slopes, depthwise=l.depthwise)
     y = torch.empty(conv.out_shape(x.shape), dtype=x.dtype, device="cuda")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(a.iters):
