@@ -317,7 +317,11 @@ def roofline(prof, works, math, peaks, steps, layers):
                 "algorithmic_bytes_per_launch": int(bytes_per_launch), "avg_launch_ms": round(avg_s * 1e3, 4),
                 "launches": launches, "peak_source": peaks["source"]}
     achieved = bytes_per_launch / avg_s / 1e9
-    return {"kernel": kind, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+    return {"kernel": kind, "bound": "hbm", "basis": "pipeline bytes: the kernel's own operand tensors (for the "
+                                                      "contraction V + U + M', i.e. the spilled transform domain; "
+                                                      "R3 reading) -- the compulsory-bytes readings R1 / R2 are "
+                                                      "in per_layer[*].roofline and roofline_step",
+            "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": traffic,
             "algorithmic_bytes_per_launch": int(bytes_per_launch), "avg_launch_ms": round(avg_s * 1e3, 4),
             "launches": launches, "peak_source": peaks["source"]}
