@@ -192,9 +192,11 @@ def kernel_work(layer, info, math, path="nested"):
             "filter_transform": {"bytes": u_b, "flops": 0},
         }
     if info.get("single_kernel"):
-        # one input channel: transform, pointwise product and output transform in one kernel;
-        # HBM traffic is x, U and y only (the kernel is bound by its CUDA-core transforms)
-        return {"fused_c1": {"bytes": x_b + u_b + y_b, "flops": 0},
+        # one input channel (fused_c1) or at most four contraction outputs (fused_co): transform,
+        # channel sum and output transform in one kernel; HBM traffic is x, U and y only (the
+        # kernel is bound by its CUDA-core transforms)
+        kind = "fused_c1" if cin_e == 1 else "fused_co"
+        return {kind: {"bytes": x_b + u_b + y_b, "flops": 0},
                 "filter_transform": {"bytes": u_b, "flops": 0}}
     return {
         "input_transform": {"bytes": x_b + v_b, "flops": 0},

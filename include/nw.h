@@ -37,7 +37,8 @@
  *    count of nw_conv_forward_host (default 8; read once, at the first host-path
  *    call or workspace query, so sizes stay consistent); NW_PDL=1 launches the
  *    three hot kernels with programmatic dependent launch; NW_FUSED_C1=0 turns
- *    off the single-kernel path for one-input-channel layers; NW_CLUSTER=1
+ *    off the single-kernel path for one-input-channel layers, NW_FUSED_CO=0 the one for
+ *    layers with at most four contraction outputs; NW_CLUSTER=1
  *    disables the CTA pairs (B multicast) of the plain contraction; NW_INPUT_TMA=0 selects
  *    the first-round input transform instead of the persistent TMA-fed kernel (bf16 x;
  *    NW_ITMA_F32=1 also fp32 x, NW_ITMA_CC=32 32 channels per task);
@@ -125,9 +126,11 @@ typedef struct {
   size_t filter_bytes; /* bytes of U for nw_transform_filter */
   int m_rows;          /* transform-domain rows per slice the contraction writes: points, or
                           P_a * l_o * m_i when the inner output level is fused into its epilogue */
-  int single_kernel;   /* 1: nw_conv_forward runs the layer as ONE kernel (one input channel: the
-                          contraction is a pointwise product, V and M stay on chip; no workspace
-                          traffic), 0: input transform, contraction, output transform */
+  int single_kernel;   /* 1: nw_conv_forward runs the layer as ONE kernel -- one input channel (the
+                          contraction is a pointwise product) or at most four contraction outputs
+                          (Cout_e <= 4: the channel sum accumulates in registers, x rows of a
+                          16-byte multiple); V and M stay on chip, HBM traffic is x and y -- 0:
+                          input transform, contraction, output transform */
 } nw_plan_info_t;
 
 /* Create a plan for a K x K convolution with the given stride (1 or 2) using

@@ -76,6 +76,14 @@ static nw_status_t forward_one(const nw_plan_st *p, const Geometry &g, const voi
     }
     return NW_OK;
   }
+  if (fused_co_eligible(p, g)) {  // Cout_e <= 4: V and M never leave the SM
+    if ((st = launch_fused_co(p, g, x, U, y, V, si)) != NW_OK) return st;
+    if (si != so) {
+      if (cudaEventRecord(e_in, si) != cudaSuccess || cudaStreamWaitEvent(so, e_in, 0) != cudaSuccess)
+        return NW_ERR_CUDA;
+    }
+    return NW_OK;
+  }
   if ((st = launch_input_transform(p, g, x, V, si)) != NW_OK) return st;
   if (p->depthwise) {  // no channel contraction: per-channel product, then the plain output transform
     if ((st = launch_depthwise_product(p, g, V, static_cast<const float *>(U), M, si)) != NW_OK) return st;

@@ -15,6 +15,8 @@ nw_status_t output_impl_pre(const nw_plan_st*, const Geometry&, const float*, vo
 
 template <int MO, int RO, int MI>
 nw_status_t fused_c1_impl(const nw_plan_st*, const Geometry&, const void*, const void*, void*, cudaStream_t);
+template <int MO, int RO, int MI>
+nw_status_t fused_co_impl(const nw_plan_st*, const Geometry&, const void*, const void*, void*, void*, cudaStream_t);
 
 #define NW_DISPATCH_AXIS(p, FN, ...)                                       \
   do {                                                                     \
@@ -56,6 +58,24 @@ bool fused_c1_eligible(const nw_plan_st* p, const Geometry& g) {
 nw_status_t launch_fused_c1(const nw_plan_st* p, const Geometry& g, const void* x, const void* U, void* y,
                             cudaStream_t s) {
   NW_DISPATCH_AXIS(p, fused_c1_impl, p, g, x, U, y, s);
+}
+
+// Single-kernel path for at most four contraction outputs (fused_smallout.cuh): C5's 9x9
+// stride-2 deconvolution (Cout_e = 4 output phases), Table I's SRCNN 5x5 1 <- 32.
+bool fused_co_eligible(const nw_plan_st* p, const Geometry& g) {
+  static const int on = [] {
+    const char* v = getenv("NW_FUSED_CO");
+    return v ? atoi(v) : 1;
+  }();
+  const long long row_bytes = (long long)g.W * (p->dtype == NW_DTYPE_BF16 ? 2 : 4);
+  return on && !p->depthwise && !p->prelu && p->math != NW_MATH_BF16 && g.path == kPathNested && g.SR == 1 &&
+         g.nph == 1 && g.mi == 3 && g.cin_e >= 2 && g.cout_e <= 4 && (g.Pa == 25 || g.Pa == 30) &&
+         row_bytes % 16 == 0;  // x windows arrive by TMA
+}
+
+nw_status_t launch_fused_co(const nw_plan_st* p, const Geometry& g, const void* x, const void* U, void* y, void* ws,
+                            cudaStream_t s) {
+  NW_DISPATCH_AXIS(p, fused_co_impl, p, g, x, U, y, ws, s);
 }
 
 }  // namespace nw

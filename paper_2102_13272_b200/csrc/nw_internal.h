@@ -116,6 +116,11 @@ nw_status_t launch_gemm_tc(const nw_plan_st *p, const Geometry &g, const void *V
 // depthwise layers: per-channel transform-domain product (depthwise.cu)
 nw_status_t launch_depthwise_product(const nw_plan_st *p, const Geometry &g, const void *V, const float *U, float *M,
                                      cudaStream_t s);
+// layers with Cout_e <= 4: the whole nested pipeline in one kernel (fused_smallout.cuh); ws holds
+// the compact U copy (Cin_e * P * 16 bytes)
+bool fused_co_eligible(const nw_plan_st *p, const Geometry &g);
+nw_status_t launch_fused_co(const nw_plan_st *p, const Geometry &g, const void *x, const void *U, void *y, void *ws,
+                            cudaStream_t s);
 // single-input-channel layers: the whole nested pipeline in one kernel (fused_small.cuh)
 bool fused_c1_eligible(const nw_plan_st *p, const Geometry &g);
 nw_status_t launch_fused_c1(const nw_plan_st *p, const Geometry &g, const void *x, const void *U, void *y,

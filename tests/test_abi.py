@@ -138,6 +138,17 @@ def test_single_kernel_for_one_input_channel():
     assert _lib.Plan(5, 1, 4, 3, 2, 32).info()["single_kernel"] == 0
 
 
+def test_single_kernel_for_four_or_fewer_outputs():
+    # Cout_e <= 4 (C5's deconvolution: 4 output phases of 1 channel; SRCNN 5x5 1 <- 32): the
+    # channel sum runs in registers, one kernel, no transform-domain rows in HBM
+    dec = _lib.Plan(9, 2, 4, 3, 32, 1, transposed=True, output_padding=1, outer_taps=0, pad=4).info()
+    assert dec["cout_e"] == 4 and dec["single_kernel"] == 1
+    assert _lib.Plan(5, 1, 4, 3, 32, 1, outer_taps=0).info()["single_kernel"] == 1
+    assert _lib.Plan(9, 1, 4, 3, 48, 3).info()["single_kernel"] == 1             # P_a 30
+    assert _lib.Plan(9, 1, 4, 3, 48, 5).info()["single_kernel"] == 0             # five outputs
+    assert _lib.Plan(9, 2, 4, 3, 8, 2, outer_taps=0).info()["single_kernel"] == 0  # stride-2 input phases
+
+
 def test_forward_argument_errors_without_touching_memory():
     # argument validation happens before any CUDA call: fake (never dereferenced) pointers suffice
     lib = _lib.load()

@@ -30,6 +30,10 @@ def test_single_kernel_layers_and_roofline_pick():
         for l, w in zip(layers, works):
             single = l.Cin == 1 and l.stride == 1 and not l.transposed
             assert ("fused_c1" in w) == single, (wl, l.name)
+            # at most four contraction outputs (C5 deconv: 4 phases, SRCNN 1 <- 32): single kernel too
+            small_out = (not single and not l.depthwise and (4 if l.transposed else 1) * l.Cout <= 4
+                         and (l.stride == 1 or l.transposed) and not l.prelu)
+            assert ("fused_co" in w) == small_out, (wl, l.name)
         # every kernel kind that launches has work attributed; the pick never divides by zero
         kinds = {k for w in works for k in w if k != "filter_transform"}
         prof = {k: (len(layers), 1.0 + i) for i, k in enumerate(sorted(kinds))}
