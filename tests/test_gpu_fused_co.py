@@ -44,9 +44,4 @@ def test_unaligned_rows_take_the_three_kernel_path():
     t, y = _run(layer, "bf16x3")
     check_parity(y, _ref(layer, t), "bf16x3", layer.dtype)
 
-
-def test_fused_small_output_full_size_deconv():
-    # BASELINE config 5's deconvolution at its full size (16 x 32 x 540 x 960 -> 1080 x 1920)
-    layer = synth.CONFIGS["c5_deconv"]
-    t, y = _run(layer, "bf16x3")
-    check_parity(y, _ref(layer, t), "bf16x3", layer.dtype)
+# the full-size C5 deconvolution runs this kernel in test_gpu_fullsize.py::test_full_size_full_tensor
