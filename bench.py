@@ -71,6 +71,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-compare", action="store_true", help="skip the OLA / direct comparison lines")
+    ap.add_argument("--layer-streams", type=int, default=1,
+                    help="1 (default): the workload's independent layers (not the c5net chain) run "
+                         "concurrently, each on its own stream and workspace; 0: one stream")
     return ap.parse_args()
 
 
@@ -492,9 +495,23 @@ def main():
         del t
     torch.cuda.synchronize()
 
+    # independent layers (not a chain) may run concurrently, each on its own stream with its own
+    # workspace: one layer's kernel tails and transforms overlap another's
+    lstreams = ([torch.cuda.Stream(device=dev) for _ in convs]
+                if args.layer_streams and not chain and len(convs) > 1 else None)
+
     def step():
-        for conv, x, y, pth in zip(convs, xs, ys, paths):
-            conv(x, y, path=pth)
+        if lstreams is None:
+            for conv, x, y, pth in zip(convs, xs, ys, paths):
+                conv(x, y, path=pth)
+            return
+        cur = torch.cuda.current_stream()
+        for st in lstreams:
+            st.wait_stream(cur)
+        for conv, x, y, pth, st in zip(convs, xs, ys, paths, lstreams):
+            conv(x, y, path=pth, stream=st)
+        for st in lstreams:
+            cur.wait_stream(st)
 
     for _ in range(args.warmup):
         step()
@@ -794,7 +811,10 @@ def main():
                        "timing": "K steps between CUDA events on the launching stream, no per-launch "
                                  "instrumentation inside; per-kernel times (roofline, kernel_ms) from a "
                                  "second instrumented pass; 'graph' = one step as a CUDA graph, median of 5",
-                       "step": "input transform + contraction + output transform per layer (nw_conv_forward)"},
+                       "step": "input transform + contraction + output transform per layer (nw_conv_forward)",
+                       "concurrency": ("the workload's independent layers run concurrently, one stream and "
+                                       "workspace each (per_layer times are each layer alone)")
+                                      if lstreams is not None else "layers in sequence on one stream"},
             "images_per_s": round(images, 1),
             "per_layer": per_layer,
             "filter_transform_ms": round(filt_ms, 4),
