@@ -500,10 +500,13 @@ def main():
     lstreams = ([torch.cuda.Stream(device=dev) for _ in convs]
                 if args.layer_streams and not chain and len(convs) > 1 else None)
 
+    def step_seq():
+        for conv, x, y, pth in zip(convs, xs, ys, paths):
+            conv(x, y, path=pth)
+
     def step():
         if lstreams is None:
-            for conv, x, y, pth in zip(convs, xs, ys, paths):
-                conv(x, y, path=pth)
+            step_seq()
             return
         cur = torch.cuda.current_stream()
         for st in lstreams:
@@ -551,10 +554,12 @@ def main():
                                        works[len(per_layer)], peaks, lm))
 
     # per-kernel times for the roofline: a second pass of K steps with every library launch
-    # bracketed by CUDA events on its stream (nw_profile_begin / end), outside the timed region
+    # bracketed by CUDA events on its stream (nw_profile_begin / end), outside the timed region;
+    # the layers run one after another here, so each launch's time is that kernel's alone (with
+    # concurrent layer streams a launch's events would also span the other layers' kernels)
     _lib.profile_begin()
     for _ in range(args.steps):
-        step()
+        step_seq()
     torch.cuda.synchronize()
     prof = _lib.profile_end()
     # SURVEY 8(d) protocol: one step captured in a CUDA graph, replayed K times, 5 repetitions,

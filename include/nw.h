@@ -40,8 +40,15 @@
  *    off the single-kernel path for one-input-channel layers, NW_FUSED_CO=0 the one for
  *    layers with at most four contraction outputs; NW_CLUSTER=1
  *    disables the CTA pairs (B multicast) of the plain contraction; NW_INPUT_TMA=0 selects
- *    the first-round input transform instead of the persistent TMA-fed kernel (bf16 x;
+ *    the first-round input transform instead of the persistent TMA-fed kernels (the
+ *    warp-specialised one, NW_ITMA_WS=0 falls back to the single-role one for bf16 x;
  *    NW_ITMA_F32=1 also fp32 x, NW_ITMA_CC=32 32 channels per task);
+ *    NW_STREAM=1|2|3 runs the input transform and the contraction (1), the contraction
+ *    and the output transform (2) or all three (3) at the same time on disjoint SM sets,
+ *    linked by per-128-slice-block completion counters in the workspace (default 0: off;
+ *    measured slower), with NW_STREAM_IT / NW_STREAM_OT CTAs for the
+ *    input / output transform (default 64 / 48) and NW_STREAM_SB blocks per sweep of the
+ *    contraction's point groups (default 1);
  *    NW_GEMM_G=g
  *    caps its 128-slice blocks per unit (default 16); NW_KBK=64 forces 64-wide
  *    K blocks for narrow layers (default: 16 / 32 when cin_pad is 16 / 32);

@@ -316,6 +316,7 @@ static nw_status_t input_launch(const Geometry& g, const void* x, void* V, cudaS
       if (g.cin_pad == 32) return input_tma_launch<MO, RO, MI, XT, 32>(g, x, V, s);
     }
   }
+  if (g.sync) return NW_ERR_UNSUPPORTED;  // the streamed pipeline needs the signalling TMA kernel
   if constexpr (BF && SR == 1) {
     if (g.vblk && g.cin_pad == 64) return input_launch_c<MO, RO, MI, SR, CC, XT, BF, 64>(g, x, V, s);
     if (g.vblk && g.cin_pad == 256) return input_launch_c<MO, RO, MI, SR, CC, XT, BF, 256>(g, x, V, s);

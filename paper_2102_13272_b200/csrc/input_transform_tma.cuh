@@ -160,8 +160,191 @@ __global__ void __launch_bounds__(ItCfg<MO, RO, MI, XT, CC_>::THREADS, ItCfg<MO,
         store_row_imm<MO, RO, MI, CINP>(za, zb, hp);
       }
     }
-    __syncthreads();  // Hs free for the next task's pass 1
+    __syncthreads();  // Hs free for the next task's pass 1 (and this task's V stores are done)
+    if (g.sync && tid == 0) {  // streamed pipeline: count (slice, source channel) completions per block
+      const long long t0 = ((long long)n * g.tiles_h + ah) * g.tiles_w + aw0;
+      const int nt = min(C::TW, g.tiles_w - aw0);
+      const long long t1 = t0 + nt - 1;
+      if ((t0 >> 7) == (t1 >> 7)) {
+        ptx::signal_add(g.sync + (t0 >> 7), nt * CC);
+      } else {
+        ptx::signal_add(g.sync + (t0 >> 7), CC);
+        ptx::signal_add(g.sync + (t1 >> 7), CC);
+      }
+    }
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Warp-specialised form (round 2, NW_ITMA_WS): the two passes of a task run on different warps
+// and overlap across tasks, so no warp waits at a CTA-wide barrier.  Per CTA (one per SM):
+//   warp P1W+P2W        TMA producer: window boxes into an NS-deep ring (mbarrier complete_tx)
+//   warps 0..P1W-1      pass 1: window s -> Hs[b] (B^T_hat along h), then release both
+//   warps P1W..+P2W-1   pass 2: Hs[b] -> split -> V stores (the same code as above)
+// Ring depths NS = 2 windows, NB = 2 Hs buffers, 16 source channels per task: pass 1 of task
+// i+1 runs while pass 2 of task i stores.  The fp32 arithmetic is the same sequence as the
+// kernels above (V bit-identical).
+template <int MO, int RO, int MI, typename XT>
+struct ItWsCfg {
+  using B = ItCfg<MO, RO, MI, XT, 16>;
+  static constexpr int P1W = 4, P2W = 12;
+  static constexpr int THREADS = (P1W + P2W + 1) * 32;
+  static constexpr int NS = 2, NB = 2;
+  static constexpr size_t SMEM = (size_t)NS * B::STAGE + (size_t)NB * B::HS * 4 + 8 * (2 * NS + 2 * NB) + 128;
+};
+
+template <int MO, int RO, int MI, typename XT, int CINP>
+__global__ void __launch_bounds__(ItWsCfg<MO, RO, MI, XT>::THREADS, 1)
+    input_transform_ws_kernel(const __grid_constant__ CUtensorMap mapX, void* __restrict__ Vout, Geometry g,
+                              int cgroups, int wgroups, int ntasks) {
+  using X = Ax<MO, RO, MI>;
+  using W = ItWsCfg<MO, RO, MI, XT>;
+  using C = typename W::B;
+  constexpr int PA = X::PA, L = X::L, CC = C::CC, NS = W::NS, NB = W::NB;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* stage = smem;                                            // NS windows
+  float* Hsb = reinterpret_cast<float*>(smem + NS * C::STAGE);            // NB x HS floats
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * C::STAGE + NB * C::HS * 4);
+  uint64_t* w_full = bars;
+  uint64_t* w_empty = bars + NS;
+  uint64_t* h_full = bars + 2 * NS;
+  uint64_t* h_empty = bars + 2 * NS + NB;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grid = gridDim.x;
+  constexpr int P1T = W::P1W * 32, P2T = W::P2W * 32;
+
+  auto decode = [&](int task, int& n, int& ah, int& wg, int& cg) {
+    int b = task;
+    cg = b % cgroups;
+    b /= cgroups;
+    wg = b % wgroups;
+    b /= wgroups;
+    ah = b % g.tiles_h;
+    n = b / g.tiles_h;
+  };
+  if (tid == 0) {
+    ptx::tma_prefetch(&mapX);
+    for (int i = 0; i < NS; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&w_full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&w_empty[i]), P1T);
+    }
+    for (int i = 0; i < NB; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&h_full[i]), P1T);
+      ptx::mbar_init(ptx::smem_u32(&h_empty[i]), P2T);
+    }
+    ptx::mbar_init_fence();
+  }
+  __syncthreads();
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();  // x may come from the previous kernel in the stream
+
+  if (warp == W::P1W + W::P2W) {  // ------------------------- TMA producer -------------------------
+    if (lane == 0) {
+      int it = 0;
+      for (int task = blockIdx.x; task < ntasks; task += grid, ++it) {
+        const int s = it % NS;
+        ptx::mbar_wait(ptx::smem_u32(&w_empty[s]), (uint32_t)(((it / NS) & 1) ^ 1));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // pass-1 reads before the refill
+        int n, ah, wg, cg;
+        decode(task, n, ah, wg, cg);
+        const int row0 = ah * X::ADV + g.off[0];
+        const int col0 = (wg * C::TW * X::ADV + g.off[0]) & ~(C::AL - 1);  // 16-byte aligned start
+        const uint32_t bar = ptx::smem_u32(&w_full[s]);
+        ptx::mbar_expect_tx(bar, (uint32_t)(CC * L * C::BW * C::ES));
+        ptx::tma_load_3d(ptx::smem_u32(stage + (size_t)s * C::STAGE), &mapX, bar, col0, row0, n * g.Cin + cg * CC);
+      }
+    }
+    return;
+  }
+  if (warp < W::P1W) {  // ------------------------- pass 1: columns along h -------------------------
+    int it = 0;
+    for (int task = blockIdx.x; task < ntasks; task += grid, ++it) {
+      const int s = it % NS, b = it % NB;
+      int n, ah, wg, cg;
+      decode(task, n, ah, wg, cg);
+      const int sh = (wg * C::TW * X::ADV + g.off[0]) & (C::AL - 1);  // window start inside the aligned box
+      const XT* win = reinterpret_cast<const XT*>(stage + (size_t)s * C::STAGE) + sh;
+      float* Hs = Hsb + (size_t)b * C::HS;
+      ptx::mbar_wait(ptx::smem_u32(&w_full[s]), (uint32_t)((it / NS) & 1));
+      ptx::mbar_wait(ptx::smem_u32(&h_empty[b]), (uint32_t)(((it / NB) & 1) ^ 1));
+#pragma unroll 1
+      for (int t1 = tid; t1 < CC * C::WC; t1 += P1T) {
+        const int col = t1 % C::WC, c = t1 / C::WC;
+        const XT* src = win + (c * L) * C::BW + col;
+        float xin[L], hv[PA];
+#pragma unroll
+        for (int r = 0; r < L; ++r) xin[r] = to_f(src[r * C::BW]);
+        in_axis<MO, RO, MI>(xin, hv);
+        float* dst = Hs + c * C::HSTR + col;
+#pragma unroll
+        for (int q = 0; q < PA; ++q) dst[q * CC * C::HSTR] = hv[q];
+      }
+      ptx::mbar_arrive(ptx::smem_u32(&w_empty[s]));
+      ptx::mbar_arrive(ptx::smem_u32(&h_full[b]));
+    }
+    return;
+  }
+  // ----------------------------- pass 2: rows along w, split, store V -----------------------------
+  const int t2 = tid - P1T, w2 = warp - W::P1W;
+  const int pair = lane % C::NPR, sub = lane / C::NPR;
+  int it = 0;
+  for (int task = blockIdx.x; task < ntasks; task += grid, ++it) {
+    const int b = it % NB;
+    int n, ah, wg, cg;
+    decode(task, n, ah, wg, cg);
+    const int aw0 = wg * C::TW;
+    const float* Hs = Hsb + (size_t)b * C::HS;
+    ptx::mbar_wait(ptx::smem_u32(&h_full[b]), (uint32_t)((it / NB) & 1));
+#pragma unroll 1
+    for (int grp = w2; grp < C::GROUPS; grp += W::P2W) {
+      const int q = grp * C::SUBS + sub;            // (p_h, tile) combo of this lane
+      const int ph = q / C::TW, tile = q % C::TW;
+      const bool live = q < C::COMBOS && aw0 + tile < g.tiles_w;
+      if (live) {
+        const float* h0 = Hs + (ph * CC + 2 * pair) * C::HSTR + tile * X::ADV;
+        const float* h1 = h0 + C::HSTR;
+        float za[X::LO][X::LI], zb[X::LO][X::LI];
+        {
+          float a[L], bb[L];
+#pragma unroll
+          for (int k = 0; k < L; ++k) {
+            a[k] = h0[k];
+            bb[k] = h1[k];
+          }
+          in_axis_inner<MO, RO, MI>(a, za);
+          in_axis_inner<MO, RO, MI>(bb, zb);
+        }
+        const long long t = ((long long)n * g.tiles_h + ah) * g.tiles_w + aw0 + tile;
+        const long long row = (((t >> 7) * g.P + (long long)ph * PA) * 2) * 128 + (t & 127);
+        char* hp = reinterpret_cast<char*>(Vout) + (row * CINP + cg * CC + 2 * pair) * 2;
+        store_row_imm<MO, RO, MI, CINP>(za, zb, hp);
+      }
+    }
+    ptx::mbar_arrive(ptx::smem_u32(&h_empty[b]));
+    if (g.sync) {  // streamed pipeline: every pass-2 thread's V stores of this task, then count them
+      asm volatile("bar.sync 1, %0;" ::"n"(P2T) : "memory");
+      if (t2 == 0) {
+        const long long t0 = ((long long)n * g.tiles_h + ah) * g.tiles_w + aw0;
+        const int nt = min(C::TW, g.tiles_w - aw0);
+        const long long t1 = t0 + nt - 1;
+        if ((t0 >> 7) == (t1 >> 7)) {
+          ptx::signal_add(g.sync + (t0 >> 7), nt * CC);
+        } else {
+          ptx::signal_add(g.sync + (t0 >> 7), CC);
+          ptx::signal_add(g.sync + (t1 >> 7), CC);
+        }
+      }
+    }
+  }
+}
+
+// NW_ITMA_WS=0|1: the warp-specialised kernel (default on; measured in profiles/r2u_*)
+inline bool input_ws_enabled() {
+  static const int on = [] {
+    const char* v = getenv("NW_ITMA_WS");
+    return v ? atoi(v) : 1;
+  }();
+  return on != 0;
 }
 
 bool encode_tmap(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base, const uint64_t* dims,
@@ -204,7 +387,8 @@ static nw_status_t input_tma_launch_cc(const Geometry& g, const void* x, void* V
   if (ntasks >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long slots = (long long)sms * C::MINB;  // persistent: every resident CTA slot
+  long long slots = (long long)sms * C::MINB;  // persistent: every resident CTA slot
+  if (g.it_ctas > 0 && g.it_ctas < slots) slots = g.it_ctas;  // streamed pipeline: its share of the SMs
   const int grid = (int)(ntasks < slots ? ntasks : slots);
   LaunchScope scope_("input_transform", s);
   if (launch_pdl(kern, dim3(grid), dim3(C::THREADS), C::SMEM, s, mapX, V, g, cgroups, wgroups, (int)ntasks) != NW_OK)
@@ -213,7 +397,43 @@ static nw_status_t input_tma_launch_cc(const Geometry& g, const void* x, void* V
 }
 
 template <int MO, int RO, int MI, typename XT, int CINP>
+static nw_status_t input_ws_launch(const Geometry& g, const void* x, void* V, cudaStream_t s) {
+  using W = ItWsCfg<MO, RO, MI, XT>;
+  using C = typename W::B;
+  auto kern = input_transform_ws_kernel<MO, RO, MI, XT, CINP>;
+  if (ensure_smem<input_transform_ws_kernel<MO, RO, MI, XT, CINP>>((int)W::SMEM) != NW_OK) return NW_ERR_CUDA;
+  const uint64_t dims[3] = {(uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.N * g.Cin};
+  const uint64_t strides[2] = {(uint64_t)g.W * C::ES, (uint64_t)g.H * g.W * C::ES};
+  const uint32_t box[3] = {(uint32_t)C::BW, (uint32_t)C::L, (uint32_t)C::CC};
+  alignas(64) CUtensorMap mapX;
+  if (!encode_tmap(&mapX, sizeof(XT) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, x,
+                   dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return NW_ERR_CUDA;
+  const int wgroups = (g.tiles_w + C::TW - 1) / C::TW;
+  const int cgroups = g.Cin / C::CC;
+  const long long ntasks = (long long)g.N * g.tiles_h * wgroups * cgroups;
+  if (ntasks >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long slots = sms;
+  if (g.it_ctas > 0 && g.it_ctas < slots) slots = g.it_ctas;
+  const int grid = (int)(ntasks < slots ? ntasks : slots);
+  LaunchScope scope_("input_transform", s);
+  if (launch_pdl(kern, dim3(grid), dim3(W::THREADS), W::SMEM, s, mapX, V, g, cgroups, wgroups, (int)ntasks) != NW_OK)
+    return NW_ERR_CUDA;
+  return check_launch();
+}
+
+// The warp-specialised kernel measured faster for the r_o = 3 outer kernels (c2k9 / c2k7 input
+// transform 0.222 -> 0.207 ms, C3 0.478 -> 0.437 ms) and slower for the mixed F(4,2) outer kernel
+// (c2k5 0.164 -> 0.168 ms, where the first-round kernel stays; profiles/r2u_workloads.md)
+template <int RO>
+constexpr bool ws_preferred() { return RO == 3; }
+
+template <int MO, int RO, int MI, typename XT, int CINP>
 static nw_status_t input_tma_launch(const Geometry& g, const void* x, void* V, cudaStream_t s) {
+  if (input_ws_enabled() && ws_preferred<RO>() && ItWsCfg<MO, RO, MI, XT>::SMEM <= 227 * 1024)
+    return input_ws_launch<MO, RO, MI, XT, CINP>(g, x, V, s);
   if (input_tma_cc() == 32 && g.Cin % 32 == 0 && ItCfg<MO, RO, MI, XT, 32>::SMEM <= 227 * 1024)
     return input_tma_launch_cc<MO, RO, MI, XT, CINP, 32>(g, x, V, s);
   return input_tma_launch_cc<MO, RO, MI, XT, CINP, 16>(g, x, V, s);
@@ -232,7 +452,7 @@ inline bool input_tma_eligible(const Geometry& g) {
     const char* v = getenv("NW_ITMA_F32");
     return v && atoi(v) == 1;
   }();
-  return input_tma_enabled() && (sizeof(XT) == 2 || fp32_too) && g.SR == 1 && g.nph == 1 && g.vblk && g.Cin == g.cin_pad && g.Cin % C::CC == 0 &&
+  return input_tma_enabled() && (sizeof(XT) == 2 || fp32_too || g.sync || (input_ws_enabled() && ws_preferred<RO>())) && g.SR == 1 && g.nph == 1 && g.vblk && g.Cin == g.cin_pad && g.Cin % C::CC == 0 &&
          ((long long)g.W * C::ES) % 16 == 0 && 2 * C::SMEM <= 227 * 1024 && g.H < (1 << 30);
 }
 

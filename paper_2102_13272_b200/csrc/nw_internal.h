@@ -45,6 +45,12 @@ struct Geometry {
   int gemm_ctas;     // persistent contraction grid (0: one CTA per SM)
   int vblk;          // V in the blocked split layout [T_pad/128][P][hi, lo][128][cin_pad] (nested, bf16x3)
   int cs;            // stride 2: ce = (2p + q) * cs + ci (phase-major contraction channels)
+  // streamed pipeline (api.cu forward_streamed): per-128-slice-block completion counters the
+  // producing kernel releases and the consuming kernel acquires (nullptr: stream-ordered launches)
+  int *sync;         // [nmb] input transform -> contraction
+  int *sync2;        // [nmb] contraction -> output transform
+  int it_ctas;       // persistent input-transform grid (0: every SM)
+  int ot_ctas;       // persistent output-transform grid (0: every SM)
 };
 
 constexpr int kPathNested = 0, kPathOla = 1, kPathDirect = 2;

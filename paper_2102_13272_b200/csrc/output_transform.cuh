@@ -374,8 +374,12 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI, PRE>::THREADS, 1)
       ptx::tma_prefetch(&mapM);
       int st = 0;
       uint32_t ph = 0;
+      int waited = -1;  // streamed pipeline: highest 128-slice block whose M' is complete
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int t0 = (u / ngroups) * C::TS, co0 = (u % ngroups) * C::CO;
+        if (g.sync2) {  // units walk the slices in order: wait for the contraction's units of t0's block
+          for (; waited < (t0 >> 7); ++waited) ptx::wait_count(g.sync2 + waited + 1, PA * LO);
+        }
         for (int r = 0; r < PA; ++r) {
           ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
           const uint32_t fb = ptx::smem_u32(&full[st]);
@@ -422,6 +426,7 @@ static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const f
   const long long nunits = tchunks * ngroups;
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (g.ot_ctas > 0 && g.ot_ctas < sms) sms = g.ot_ctas;  // streamed pipeline: its share of the SMs
   const int grid = (int)(nunits < sms ? nunits : sms);
   LaunchScope scope_("output_transform", s);
   if (launch_pdl(kern, dim3(grid), dim3(C::THREADS), C::SMEM, s, map, static_cast<YT*>(y), g,

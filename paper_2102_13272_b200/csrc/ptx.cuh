@@ -18,6 +18,28 @@ __device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uin
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(b - hb), "f"(a - ha));
 }
 
+// Cross-kernel completion counters of the streamed pipeline.  A producer CTA, after a CTA
+// barrier that orders all of its threads' global stores before this thread, makes them visible
+// to the async proxy (the consumer reads them with TMA) and releases them with the count.
+__device__ __forceinline__ void signal_add(int* c, int v) {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(c), "r"(v) : "memory");
+}
+// Consumer: spin (with back-off) until *c >= expect, acquire, then order the acquired data
+// before this thread's later async-proxy (TMA) reads.  ~4 s without progress traps (a missing
+// producer would otherwise hang the GPU).
+__device__ __forceinline__ void wait_count(const int* c, int expect) {
+  int v;
+  long long spins = 0;
+  while (true) {
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+    if (v >= expect) break;
+    __nanosleep(128);
+    if (++spins > (1ll << 25)) __trap();
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -360,9 +360,31 @@ struct FusedParams {
   long long a_lo_row, b_lo_row;
   int P, vblk;
   float* Mp;
+  // streamed pipeline (api.cu forward_streamed): units walk 128-slice blocks in order (sb blocks
+  // per sweep of the point groups, so one U point group serves sb blocks back to back); before
+  // the first V load of block mb the producer waits for ready[mb] >= rdy_per_slice * (real
+  // slices of mb); each finished unit adds 1 to done[mb] for the output transform.
+  const int* ready;
+  int* done;
+  int rdy_per_slice, sb;
+  long long T;
 };
 
-template <int MI>
+// unit u -> (point group pg = p_h * l_o + p_o, 128-slice block mb)
+__device__ __forceinline__ void fused_unit(const FusedParams& p, int u, int& pg, int& mb) {
+  const int PG = p.PA * p.LO;
+  if (p.sb <= 0) {  // point-group major (stream-ordered launches)
+    pg = u / p.nmb;
+    mb = u - pg * p.nmb;
+    return;
+  }
+  const int gsz = p.sb * PG, grp = u / gsz, r = u - grp * gsz, mb0 = grp * p.sb;
+  const int nb = min(p.sb, p.nmb - mb0);
+  pg = r / nb;
+  mb = mb0 + (r - pg * nb);
+}
+
+template <int MI, int NH>
 __global__ void __launch_bounds__(kFuseThreads, 1)
     contraction_fused_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapU,
                              const FusedParams p) {
@@ -408,9 +430,18 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
     if (lane == 0) {  // ------------------------- TMA producer -------------------------
       int st = 0;
       uint32_t ph = 0;
+      int waited = -1;  // highest block whose V is known complete
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int pg = u / p.nmb, mb = u - pg * p.nmb;
+        int pg, mb;
+        fused_unit(p, u, pg, mb);
         const int p_h = pg / p.LO, p_o = pg - p_h * p.LO;
+        if (p.ready) {  // every block of this unit's sweep group (units walk the groups in order)
+          const int gsz = p.sb * p.PA * p.LO, last = min(p.nmb, (u / gsz + 1) * p.sb) - 1;
+          for (; waited < last; ++waited) {
+            const long long s0 = (long long)(waited + 1) * kBM, s1 = min(p.T, s0 + kBM);
+            ptx::wait_count(p.ready + waited + 1, p.rdy_per_slice * (int)(s1 - s0));
+          }
+        }
         for (int pi = 0; pi < LI; ++pi) {
           const int xi = p_h * p.PA + p_o * LI + pi;
           for (int kb = 0; kb < p.KB; ++kb) {
@@ -470,10 +501,11 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
     }
   } else {  // ------------------------------- epilogue ----------------------------------
     const int q = warp & 3, half = (warp - 2) >> 2;
-    const int NH = p.N >> 1;               // 16 or 32 columns per warp
+    static_assert(NH == 16 || NH == 32, "16 or 32 columns per warp (N = 32 or 64)");
     uint32_t sc = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int pg = u / p.nmb, mb = u - pg * p.nmb;
+      int pg, mb;
+      fused_unit(p, u, pg, mb);
       float out[MI][32];
 #pragma unroll
       for (int s = 0; s < MI; ++s)
@@ -505,12 +537,28 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
         }
       }
       const long long t = (long long)mb * kBM + q * 32 + lane;
+      // one pointer walked by the channel pitch (T_pad floats): one 64-bit add per store instead
+      // of a 64-bit multiply-add chain (the epilogue's address arithmetic was half of the kernel's
+      // instructions and kept the MMA waiting for TMEM slots; profiles/r2u)
+      float* dst = p.Mp + ((long long)(pg * MI) * p.N + half * NH) * p.T_pad + t;
+      const long long pitch = p.T_pad;
+      const long long skip = (long long)(p.N - NH) * p.T_pad;  // to the next s row's first column
 #pragma unroll
       for (int s = 0; s < MI; ++s) {
-        float* dst = p.Mp + ((long long)(pg * MI + s) * p.N + half * NH) * p.T_pad + t;
 #pragma unroll
-        for (int c = 0; c < 32; ++c)
-          if (c < NH) dst[(long long)c * p.T_pad] = out[s][c];
+        for (int c = 0; c < NH; ++c) {
+          *dst = out[s][c];
+          long long w = pitch;
+          asm volatile("" : "+l"(w));  // keep the walk incremental (no hoisted per-store offsets)
+          dst += w;
+        }
+        long long w = skip;
+        asm volatile("" : "+l"(w));
+        dst += w;
+      }
+      if (p.done) {  // streamed pipeline: the 8 epilogue warps' M' stores of this unit, then count it
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (warp == 2 && lane == 0) ptx::signal_add(p.done + mb, 1);
       }
     }
   }
@@ -669,6 +717,15 @@ nw_status_t launch_gemm_tc_fused(const nw_plan_st* p, const Geometry& g, const v
   prm.P = g.P;
   prm.vblk = (g.vblk && prm.lo) ? 1 : 0;
   prm.Mp = Mp;
+  prm.ready = g.sync;
+  prm.done = g.sync2;
+  prm.rdy_per_slice = g.Cin;  // the input transform counts (slice, source channel) pairs
+  prm.T = g.T;
+  static const int sb_env = [] {
+    const char* v = getenv("NW_STREAM_SB");
+    return v ? atoi(v) : 1;
+  }();
+  prm.sb = (g.sync || g.sync2) ? (sb_env > 0 ? sb_env : 1) : 0;
   const uint32_t stage = (tc::kBM * prm.kbk * 2 + (uint32_t)prm.N * prm.kbk * 2) * (prm.lo ? 2 : 1);
   prm.nst = (int)((200u * 1024u) / stage);
   if (prm.nst > tc::kMaxStages) prm.nst = tc::kMaxStages;
@@ -680,11 +737,14 @@ nw_status_t launch_gemm_tc_fused(const nw_plan_st* p, const Geometry& g, const v
   alignas(64) CUtensorMap mapV, mapU;
   if (!make_map(&mapV, V, rowsV, g.cin_pad, tc::kBM, prm.kbk)) return NW_ERR_CUDA;
   if (!make_map(&mapU, U, rowsU, g.cin_pad, prm.N, prm.kbk)) return NW_ERR_CUDA;
-  auto kern = tc::contraction_fused_kernel<3>;
-  if (ensure_smem<tc::contraction_fused_kernel<3>>(227 * 1024) != NW_OK) return NW_ERR_CUDA;
+  auto kern = prm.N == 64 ? tc::contraction_fused_kernel<3, 32> : tc::contraction_fused_kernel<3, 16>;
+  if ((prm.N == 64 ? ensure_smem<tc::contraction_fused_kernel<3, 32>>(227 * 1024)
+                   : ensure_smem<tc::contraction_fused_kernel<3, 16>>(227 * 1024)) != NW_OK)
+    return NW_ERR_CUDA;
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long units = (long long)prm.nmb * prm.PA * prm.LO;
+  if (g.gemm_ctas > 0 && g.gemm_ctas < sms) sms = g.gemm_ctas;
   const int grid = (int)(units < sms ? units : sms);
   LaunchScope scope_("contraction_tc", s);
   if (launch_pdl(kern, dim3(grid), dim3(tc::kFuseThreads), smem, s, mapV, mapU, prm) != NW_OK) return NW_ERR_CUDA;

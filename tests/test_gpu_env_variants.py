@@ -67,6 +67,18 @@ BITWISE = [
      {"NW_INPUT_TMA": "0"}),
     ({"config": "c2k9", "N": 3, "H": 50, "W": 48, "Cin": 64, "Cout": 32, "m_o": 3, "dtype": "bf16"},
      {"NW_INPUT_TMA": "0"}),
+    # warp-specialised TMA input transform (default for r_o = 3, fp32 and bf16 x) vs the first-round
+    # kernel (fp32) and the single-role TMA kernel (bf16)
+    ({**C2, "N": 9, "H": 64, "W": 64}, {"NW_ITMA_WS": "0"}),
+    ({**C2, "W": 56}, {"NW_ITMA_WS": "0"}),
+    ({**C3, "N": 6, "H": 64, "W": 64}, {"NW_ITMA_WS": "0"}),
+    # streamed pipeline: kernels on disjoint SM sets linked by completion counters; 9 x 36 slices =
+    # three 128-slice blocks, the last one partial
+    ({**C2, "N": 9, "H": 64, "W": 64}, {"NW_STREAM": "1"}),
+    ({**C2, "N": 9, "H": 64, "W": 64}, {"NW_STREAM": "2"}),
+    ({**C2, "N": 9, "H": 64, "W": 64}, {"NW_STREAM": "3", "NW_STREAM_SB": "2"}),
+    ({**C2, "N": 9, "H": 64, "W": 64, "dtype": "bf16"}, {"NW_STREAM": "3"}),
+    ({**C2, "config": "c2k5", "N": 9, "H": 64, "W": 64}, {"NW_STREAM": "3", "NW_STREAM_IT": "40"}),
 ]
 
 

@@ -1,0 +1,16 @@
+#!/bin/bash
+# ncu --set full (with source) of the c2k9 contraction and the warp-specialised input transform
+TAG=r2u
+mkdir -p gpurun_out
+timeout 120 python tools/prof_layer.py c2k9 > /dev/null 2>&1
+for K in contraction input_transform_ws; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 \
+    -o gpurun_out/prof_${TAG}_c2k9_$K python tools/prof_layer.py c2k9 > gpurun_out/ncu_${TAG}_$K.log 2>&1; echo "ncu $K rc=$?"
+done
+for r in gpurun_out/prof_${TAG}_*.ncu-rep; do
+  b=$(basename $r .ncu-rep)
+  ncu -i $r --page raw --csv > gpurun_out/$b.raw.csv 2>/dev/null
+  ncu -i $r --page source --csv > gpurun_out/$b.source.csv 2>/dev/null
+  ncu -i $r --page details --csv > gpurun_out/$b.details.csv 2>/dev/null
+done
+ls gpurun_out | grep $TAG

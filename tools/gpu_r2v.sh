@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/r2v_pt.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/r2v_pt.log
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/r2v_bench.json 2> gpurun_out/r2v_bench.err; echo "bench rc=$?"
+python -c "
+import json;d=json.load(open('gpurun_out/r2v_bench.json'));print(d['value'],d['ms_per_step'],d.get('graph'),d['roofline']['frac'],d['roofline']['avg_launch_ms']); print([(p['layer'],p['ms']) for p in d['per_layer']]); print(d['e2e'])"
