@@ -102,6 +102,33 @@ __device__ __forceinline__ void store_row_imm(const float (*za)[Ax<MO, RO, MI>::
   }
 }
 
+// Packed form of store_row_imm: lane 0 of each f2 is channel a, lane 1 channel b; the split's
+// subtraction runs on both channels at once (same per-lane rounding as split_bf16x2).
+template <int MO, int RO, int MI, int CINP>
+__device__ __forceinline__ void store_row_imm_p(const f2 (*zab)[Ax<MO, RO, MI>::LI], char* hp) {
+  using X = Ax<MO, RO, MI>;
+  constexpr long long PS = 2ll * 128 * CINP * 2, PL = 128ll * CINP * 2;
+#pragma unroll
+  for (int pi = 0; pi < X::LI; ++pi) {
+    f2 o[X::LO];
+    in_axis_outer_col_t<MO, RO, MI, f2>(zab, pi, o);
+#pragma unroll
+    for (int po = 0; po < X::LO; ++po) {
+      float a, b;
+      f2_unpack(o[po], a, b);
+      uint32_t hi, lo;
+      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(b), "f"(a));
+      const f2 r = o[po] - f2_pack(__uint_as_float(hi << 16), __uint_as_float(hi & 0xffff0000u));
+      float ra, rb;
+      f2_unpack(r, ra, rb);
+      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(rb), "f"(ra));
+      char* h = hp + (po * X::LI + pi) * PS;
+      *reinterpret_cast<uint32_t*>(h) = hi;
+      *reinterpret_cast<uint32_t*>(h + PL) = lo;
+    }
+  }
+}
+
 }  // namespace nw
 
 #include "input_transform_tma.cuh"  // persistent TMA-fed kernel (uses store_row_imm)

@@ -267,17 +267,46 @@ __global__ void __launch_bounds__(ItWsCfg<MO, RO, MI, XT>::THREADS, 1)
       float* Hs = Hsb + (size_t)b * C::HS;
       ptx::mbar_wait(ptx::smem_u32(&w_full[s]), (uint32_t)((it / NS) & 1));
       ptx::mbar_wait(ptx::smem_u32(&h_empty[b]), (uint32_t)(((it / NB) & 1) ^ 1));
+      if constexpr (kPackedAxis<MO, RO, MI>) {
+        // two window columns per thread in one packed register pair (FADD2 / FFMA2)
 #pragma unroll 1
-      for (int t1 = tid; t1 < CC * C::WC; t1 += P1T) {
-        const int col = t1 % C::WC, c = t1 / C::WC;
-        const XT* src = win + (c * L) * C::BW + col;
-        float xin[L], hv[PA];
+        for (int t1 = tid; t1 < CC * C::WC; t1 += 2 * P1T) {
+          const int tb = t1 + P1T;
+          const int col = t1 % C::WC, c = t1 / C::WC;
+          const XT* src = win + (c * L) * C::BW + col;
+          float* dst = Hs + c * C::HSTR + col;
+          if (tb < CC * C::WC) {
+            const int colb = tb % C::WC, cb = tb / C::WC;
+            const XT* srcb = win + (cb * L) * C::BW + colb;
+            float* dstb = Hs + cb * C::HSTR + colb;
+            f2 xin[L], hv[PA];
 #pragma unroll
-        for (int r = 0; r < L; ++r) xin[r] = to_f(src[r * C::BW]);
-        in_axis<MO, RO, MI>(xin, hv);
-        float* dst = Hs + c * C::HSTR + col;
+            for (int r = 0; r < L; ++r) xin[r] = f2_pack(to_f(src[r * C::BW]), to_f(srcb[r * C::BW]));
+            in_axis_t<MO, RO, MI, f2>(xin, hv);
 #pragma unroll
-        for (int q = 0; q < PA; ++q) dst[q * CC * C::HSTR] = hv[q];
+            for (int q = 0; q < PA; ++q) f2_unpack(hv[q], dst[q * CC * C::HSTR], dstb[q * CC * C::HSTR]);
+          } else {
+            float xin[L], hv[PA];
+#pragma unroll
+            for (int r = 0; r < L; ++r) xin[r] = to_f(src[r * C::BW]);
+            in_axis<MO, RO, MI>(xin, hv);
+#pragma unroll
+            for (int q = 0; q < PA; ++q) dst[q * CC * C::HSTR] = hv[q];
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int t1 = tid; t1 < CC * C::WC; t1 += P1T) {
+          const int col = t1 % C::WC, c = t1 / C::WC;
+          const XT* src = win + (c * L) * C::BW + col;
+          float xin[L], hv[PA];
+#pragma unroll
+          for (int r = 0; r < L; ++r) xin[r] = to_f(src[r * C::BW]);
+          in_axis<MO, RO, MI>(xin, hv);
+          float* dst = Hs + c * C::HSTR + col;
+#pragma unroll
+          for (int q = 0; q < PA; ++q) dst[q * CC * C::HSTR] = hv[q];
+        }
       }
       ptx::mbar_arrive(ptx::smem_u32(&w_empty[s]));
       ptx::mbar_arrive(ptx::smem_u32(&h_full[b]));
@@ -303,21 +332,32 @@ __global__ void __launch_bounds__(ItWsCfg<MO, RO, MI, XT>::THREADS, 1)
       if (live) {
         const float* h0 = Hs + (ph * CC + 2 * pair) * C::HSTR + tile * X::ADV;
         const float* h1 = h0 + C::HSTR;
-        float za[X::LO][X::LI], zb[X::LO][X::LI];
-        {
-          float a[L], bb[L];
-#pragma unroll
-          for (int k = 0; k < L; ++k) {
-            a[k] = h0[k];
-            bb[k] = h1[k];
-          }
-          in_axis_inner<MO, RO, MI>(a, za);
-          in_axis_inner<MO, RO, MI>(bb, zb);
-        }
         const long long t = ((long long)n * g.tiles_h + ah) * g.tiles_w + aw0 + tile;
         const long long row = (((t >> 7) * g.P + (long long)ph * PA) * 2) * 128 + (t & 127);
         char* hp = reinterpret_cast<char*>(Vout) + (row * CINP + cg * CC + 2 * pair) * 2;
-        store_row_imm<MO, RO, MI, CINP>(za, zb, hp);
+        if constexpr (kPackedAxis<MO, RO, MI>) {  // the pair's two channels in one packed lane pair
+          f2 zab[X::LO][X::LI];
+          {
+            f2 ab[L];
+#pragma unroll
+            for (int k = 0; k < L; ++k) ab[k] = f2_pack(h0[k], h1[k]);
+            in_axis_inner_t<MO, RO, MI, f2>(ab, zab);
+          }
+          store_row_imm_p<MO, RO, MI, CINP>(zab, hp);
+        } else {
+          float za[X::LO][X::LI], zb[X::LO][X::LI];
+          {
+            float a[L], bb[L];
+#pragma unroll
+            for (int k = 0; k < L; ++k) {
+              a[k] = h0[k];
+              bb[k] = h1[k];
+            }
+            in_axis_inner<MO, RO, MI>(a, za);
+            in_axis_inner<MO, RO, MI>(bb, zb);
+          }
+          store_row_imm<MO, RO, MI, CINP>(za, zb, hp);
+        }
       }
     }
     ptx::mbar_arrive(ptx::smem_u32(&h_empty[b]));

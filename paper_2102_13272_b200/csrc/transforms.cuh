@@ -27,11 +27,52 @@ struct Ax {
 };
 
 // ---------------------------------------------------------------------------
+// f2: two fp32 lanes in one 64-bit register, operated on by Blackwell's packed fp32
+// instructions (add / sub / fma .rn.f32x2 -> SASS FADD2 / FFMA2).  Each lane is rounded exactly
+// like the scalar instruction, so a packed transform of two independent columns gives the same
+// bits as two scalar ones while issuing half the instructions (measured: FFMA2 sustains the
+// same fp32 rate as FFMA, tools/ffma2_bench.cu).  Only add, sub and fma are provided (no
+// separate multiply that ptxas could contract differently from the scalar code).
+// ---------------------------------------------------------------------------
+struct f2 {
+  unsigned long long v;
+};
+__device__ __forceinline__ f2 f2_pack(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(f2 x, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(x.v));
+}
+__device__ __forceinline__ f2 f2_splat(float c) { return f2_pack(c, c); }
+// the scalar fmaf stays visible next to the packed overload inside namespace nw
+__device__ __forceinline__ float fmaf(float c, float x, float y) { return ::fmaf(c, x, y); }
+__device__ __forceinline__ f2 operator+(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 operator-(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+// -a as (-0) - a: exact, including the sign of zero
+__device__ __forceinline__ f2 operator-(f2 a) { return f2_splat(-0.f) - a; }
+__device__ __forceinline__ f2 fmaf(float c, f2 x, f2 y) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(f2_splat(c).v), "l"(x.v), "l"(y.v));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
 // one-level 1-D kernels: out[l] = B^T in[l] (l = m + r - 1), out[m] = A^T in[l]
 // ---------------------------------------------------------------------------
 template <int M, int R>
 struct K1 {
   static constexpr int L = M + R - 1;
+  static constexpr bool kPackedBt = false;  // scalar only (generic coefficient loop)
   __device__ __forceinline__ static void bt(const float (&x)[L], float (&o)[L]) {
     constexpr Kernel1D K = make_kernel(M, R);
 #pragma unroll
@@ -76,8 +117,10 @@ struct K1 {
 template <>
 struct K1<3, 3> {
   static constexpr int L = 5;
-  __device__ __forceinline__ static void bt(const float (&x)[5], float (&o)[5]) {
-    const float a = x[3] - x[1];                         // row 3
+  static constexpr bool kPackedBt = true;  // bt accepts f2 (packed pairs of columns)
+  template <typename T>
+  __device__ __forceinline__ static void bt(const T (&x)[5], T (&o)[5]) {
+    const T a = x[3] - x[1];                             // row 3
     o[3] = a;
     o[0] = fmaf(2.f, x[0] - x[2], a);                    // 2x0 - x1 - 2x2 + x3
     o[1] = (x[1] + x[2]) - a;                            // 2x1 + x2 - x3
@@ -98,10 +141,12 @@ struct K1<3, 3> {
 template <>
 struct K1<4, 3> {
   static constexpr int L = 6;
-  __device__ __forceinline__ static void bt(const float (&x)[6], float (&o)[6]) {
-    const float a = fmaf(-4.f, x[2], x[4]);              // x4 - 4x2
-    const float b = fmaf(-4.f, x[1], x[3]);              // x3 - 4x1
-    const float c = x[4] - x[2], d = x[3] - x[1];
+  static constexpr bool kPackedBt = true;
+  template <typename T>
+  __device__ __forceinline__ static void bt(const T (&x)[6], T (&o)[6]) {
+    const T a = fmaf(-4.f, x[2], x[4]);                  // x4 - 4x2
+    const T b = fmaf(-4.f, x[1], x[3]);                  // x3 - 4x1
+    const T c = x[4] - x[2], d = x[3] - x[1];
     o[0] = fmaf(4.f, x[0], fmaf(-5.f, x[2], x[4]));      // 4x0 - 5x2 + x4
     o[1] = -a - b;                                       // 4x1 + 4x2 - x3 - x4
     o[2] = b - a;                                        // -4x1 + 4x2 + x3 - x4
@@ -145,7 +190,9 @@ static_assert(bt_equal(4, 2, 3, 3) && at_equals<4, 5>(2, kAT42), "F(4,2) tables"
 template <>
 struct K1<4, 2> {
   static constexpr int L = 5;
-  __device__ __forceinline__ static void bt(const float (&x)[5], float (&o)[5]) { K1<3, 3>::bt(x, o); }
+  static constexpr bool kPackedBt = true;
+  template <typename T>
+  __device__ __forceinline__ static void bt(const T (&x)[5], T (&o)[5]) { K1<3, 3>::bt(x, o); }
   __device__ __forceinline__ static void at(const float (&x)[5], float (&o)[4]) {
     const float s = x[1] + x[2], d = x[1] - x[2];
     o[0] = (x[0] + x[3]) + s;                            // x0 + x1 + x2 + x3
@@ -163,7 +210,9 @@ static_assert(bt_equal(5, 2, 4, 3) && at_equals<5, 6>(2, kAT52), "F(5,2) tables"
 template <>
 struct K1<5, 2> {
   static constexpr int L = 6;
-  __device__ __forceinline__ static void bt(const float (&x)[6], float (&o)[6]) { K1<4, 3>::bt(x, o); }
+  static constexpr bool kPackedBt = true;
+  template <typename T>
+  __device__ __forceinline__ static void bt(const T (&x)[6], T (&o)[6]) { K1<4, 3>::bt(x, o); }
   __device__ __forceinline__ static void at(const float (&x)[6], float (&o)[5]) {
     const float s1 = x[1] + x[2], d1 = x[1] - x[2], s2 = x[3] + x[4], d2 = x[3] - x[4];
     o[0] = (x[0] + s1) + s2;                             // x0 + x1 + x2 + x3 + x4
@@ -217,6 +266,46 @@ __device__ __forceinline__ void in_axis(const float* x, float* v) {
   for (int pi = 0; pi < X::LI; ++pi) {
     float o[X::LO];
     in_axis_outer_col<MO, RO, MI>(z, pi, o);
+#pragma unroll
+    for (int po = 0; po < X::LO; ++po) v[po * X::LI + pi] = o[po];
+  }
+}
+
+// the same three functions on any value type T the 1-D kernels accept (float or f2); packed
+// forms exist when both levels' B^T are hand-factored (kPackedAxis)
+template <int MO, int RO, int MI>
+constexpr bool kPackedAxis = K1<MO, RO>::kPackedBt && K1<MI, kRi>::kPackedBt;
+template <int MO, int RO, int MI, typename T>
+__device__ __forceinline__ void in_axis_inner_t(const T* x, T (*z)[Ax<MO, RO, MI>::LI]) {
+  using X = Ax<MO, RO, MI>;
+#pragma unroll
+  for (int j = 0; j < X::LO; ++j) {
+    T col[X::LI], o[X::LI];
+#pragma unroll
+    for (int s = 0; s < X::LI; ++s) col[s] = x[kRi * j + s];
+    K1<MI, kRi>::bt(col, o);
+#pragma unroll
+    for (int s = 0; s < X::LI; ++s) z[j][s] = o[s];
+  }
+}
+template <int MO, int RO, int MI, typename T>
+__device__ __forceinline__ void in_axis_outer_col_t(const T (*z)[Ax<MO, RO, MI>::LI], int pi,
+                                                    T (&o)[Ax<MO, RO, MI>::LO]) {
+  using X = Ax<MO, RO, MI>;
+  T c[X::LO];
+#pragma unroll
+  for (int j = 0; j < X::LO; ++j) c[j] = z[j][pi];
+  K1<MO, RO>::bt(c, o);
+}
+template <int MO, int RO, int MI, typename T>
+__device__ __forceinline__ void in_axis_t(const T* x, T* v) {
+  using X = Ax<MO, RO, MI>;
+  T z[X::LO][X::LI];
+  in_axis_inner_t<MO, RO, MI, T>(x, z);
+#pragma unroll
+  for (int pi = 0; pi < X::LI; ++pi) {
+    T o[X::LO];
+    in_axis_outer_col_t<MO, RO, MI, T>(z, pi, o);
 #pragma unroll
     for (int po = 0; po < X::LO; ++po) v[po * X::LI + pi] = o[po];
   }
