@@ -3,6 +3,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import os
+import re
 import shutil
 import subprocess
 import sys
@@ -39,14 +40,33 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+_INC = re.compile(r'^\s*#\s*include\s+"([^"]+)"', re.M)
+
+
+def _deps(path: str, seen=None) -> set:
+    """Local headers a source includes, recursively (quoted includes under csrc/ and include/)."""
+    seen = set() if seen is None else seen
+    for name in _INC.findall(open(path).read()):
+        for d in (os.path.dirname(path), CSRC, os.path.join(os.path.dirname(HERE), "include")):
+            h = os.path.normpath(os.path.join(d, name))
+            if os.path.exists(h):
+                if h not in seen:
+                    seen.add(h)
+                    _deps(h, seen)
+                break
+    return seen
+
+
 def _stale(src: str, headers_mtime: float) -> bool:
-    """An object is rebuilt when its .cu, any header (.cuh / .h, incl. include/nw.h) or this
-    script is newer than it (headers are shared by most translation units)."""
+    """An object is rebuilt when its .cu, a header it includes (recursively) or this script is
+    newer than it."""
     obj = os.path.join(BUILD, src.replace(".cu", ".o"))
     if not os.path.exists(obj):
         return True
     t = os.path.getmtime(obj)
-    return os.path.getmtime(os.path.join(CSRC, src)) > t or headers_mtime > t
+    path = os.path.join(CSRC, src)
+    newest = max([os.path.getmtime(path), os.path.getmtime(__file__)] + [os.path.getmtime(h) for h in _deps(path)])
+    return newest > t
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

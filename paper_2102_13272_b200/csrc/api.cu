@@ -142,7 +142,7 @@ static nw_status_t forward_one(const nw_plan_st *p, const Geometry &g, const voi
     if (done) return NW_OK;
   }
   if (fused_c1_eligible(p, g)) {  // one input channel: V and M never leave the SM
-    if ((st = launch_fused_c1(p, g, x, U, y, si)) != NW_OK) return st;
+    if ((st = launch_fused_c1(p, g, x, U, y, V, v_bytes(p, g), si)) != NW_OK) return st;
     if (si != so) {
       if (cudaEventRecord(e_in, si) != cudaSuccess || cudaStreamWaitEvent(so, e_in, 0) != cudaSuccess)
         return NW_ERR_CUDA;

@@ -14,7 +14,7 @@ template <int MO, int RO, int MI>
 nw_status_t output_impl_pre(const nw_plan_st*, const Geometry&, const float*, void*, cudaStream_t);
 
 template <int MO, int RO, int MI>
-nw_status_t fused_c1_impl(const nw_plan_st*, const Geometry&, const void*, const void*, void*, cudaStream_t);
+nw_status_t fused_c1_impl(const nw_plan_st*, const Geometry&, const void*, const void*, void*, void*, cudaStream_t);
 template <int MO, int RO, int MI>
 nw_status_t fused_co_impl(const nw_plan_st*, const Geometry&, const void*, const void*, void*, void*, cudaStream_t);
 
@@ -55,9 +55,16 @@ bool fused_c1_eligible(const nw_plan_st* p, const Geometry& g) {
          g.Pa <= 30;  // V of 32 slices in shared memory: up to F(4,3) / F(5,2) (x) F(3,3)
 }
 
+// fp32 U per channel group, [group][CO][P_a][P_a rounded up to even]: at most 16 channels of
+// padding and one float of row padding
+size_t fused_c1_ws_bytes(const nw_plan_st* p, const Geometry& g) {
+  (void)p;
+  return (size_t)((g.cout_e + 15) / 16 * 16) * g.Pa * (g.Pa + 1) * 4;
+}
+
 nw_status_t launch_fused_c1(const nw_plan_st* p, const Geometry& g, const void* x, const void* U, void* y,
-                            cudaStream_t s) {
-  NW_DISPATCH_AXIS(p, fused_c1_impl, p, g, x, U, y, s);
+                            void* ws, size_t ws_bytes, cudaStream_t s) {
+  NW_DISPATCH_AXIS(p, fused_c1_impl, p, g, x, U, y, ws_bytes >= fused_c1_ws_bytes(p, g) ? ws : nullptr, s);
 }
 
 // Single-kernel path for at most four contraction outputs (fused_smallout.cuh): C5's 9x9

@@ -13,6 +13,9 @@
 
 namespace nw {
 
+template <int MO, int RO, int MI>
+constexpr int X_PA() { return Ax<MO, RO, MI>::PA; }
+
 template <int MO, int RO, int MI, int CO_>
 struct FusedC1Shape {
   using X = Ax<MO, RO, MI>;
@@ -33,8 +36,38 @@ struct FusedC1Shape {
   static constexpr size_t U_BYTES = (size_t)CO * X::PA * RPU * 4;
   static constexpr size_t INFO_BYTES = (size_t)WARPS * 32 * 16;
   static constexpr size_t HS_OR_STAGE = H_BYTES > STAGE_BYTES ? H_BYTES : STAGE_BYTES;
-  static constexpr size_t SMEM = 128 + V_BYTES + HS_OR_STAGE + U_BYTES + INFO_BYTES;
+  // U of the current and, where shared memory allows, the next channel group (bulk copies from
+  // the prepped fp32 copy; one buffer: the copy is issued and awaited at the group's start)
+  static constexpr size_t SMEM1 = 128 + V_BYTES + HS_OR_STAGE + U_BYTES + INFO_BYTES + 16;
+  static constexpr int NUB = (SMEM1 + U_BYTES <= 227 * 1024) ? 2 : 1;
+  static constexpr size_t SMEM = SMEM1 + (NUB - 1) * U_BYTES;
 };
+
+// U (plan layout [P][cout_pad][cin_pad], fp32 or bf16 hi / lo planes) -> Uc, one contiguous block
+// per channel group in exactly the shared-memory layout of Us: [group][CO][p_h][RPU] fp32 (zero
+// for channels >= Cout_e and the row padding), so the kernel stages a group with one bulk copy
+static __global__ void fused_c1_prep_kernel(const void* __restrict__ U, int umode, float* __restrict__ Uc, int PA, int RPU,
+                                     int CO, int ngroups, int cout_e, int cout_pad, int cin_pad) {
+  const long long n = (long long)ngroups * CO * PA * RPU;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int pw = (int)(i % RPU);
+  long long r = i / RPU;
+  const int ph = (int)(r % PA);
+  const int co = (int)(r / PA);  // group * CO + cl
+  float u = 0.f;
+  if (co < cout_e && pw < PA) {
+    const long long P = (long long)PA * PA;
+    const long long o = ((long long)(ph * PA + pw) * cout_pad + co) * cin_pad;  // input channel 0
+    if (umode) {  // 1: bf16 hi + lo planes, 2: hi only
+      const __nv_bfloat16* Ub = static_cast<const __nv_bfloat16*>(U);
+      u = __bfloat162float(Ub[o]) + (umode == 1 ? __bfloat162float(Ub[P * cout_pad * cin_pad + o]) : 0.f);
+    } else {
+      u = static_cast<const float*>(U)[o];
+    }
+  }
+  Uc[i] = u;
+}
 
 // Warps per CTA: the consumers are latency-bound, so as many as registers allow -- 16 (128
 // registers) for the column-split 12 x 12 tile, 12 (168) for a 9 x 9 tile held whole (16 spill)
@@ -50,8 +83,8 @@ struct FusedC1Cfg
 
 template <int MO, int RO, int MI, typename XT, typename YT>
 __global__ void __launch_bounds__(FusedC1Cfg<MO, RO, MI>::THREADS, 1)
-    fused_c1_kernel(const XT* __restrict__ x, const void* __restrict__ Uraw, int umode, YT* __restrict__ y,
-                    Geometry g, const float* __restrict__ slopes, int nchunks) {
+    fused_c1_kernel(const XT* __restrict__ x, const void* __restrict__ Uraw, const float* __restrict__ Uc, int umode,
+                    YT* __restrict__ y, Geometry g, const float* __restrict__ slopes, int nchunks) {
   using X = Ax<MO, RO, MI>;
   using C = FusedC1Cfg<MO, RO, MI>;
   using O = OutCfg<MO, RO, MI, false>;
@@ -60,11 +93,36 @@ __global__ void __launch_bounds__(FusedC1Cfg<MO, RO, MI>::THREADS, 1)
   uint8_t* base = smem_raw + ((128u - (ptx::smem_u32(smem_raw) & 127u)) & 127u);
   float* Vs = reinterpret_cast<float*>(base);
   float* Hs = reinterpret_cast<float*>(base + C::V_BYTES);      // pass 1, then the output stage
-  float* Us = reinterpret_cast<float*>(base + C::V_BYTES + C::HS_OR_STAGE);
-  long long* sinfo = reinterpret_cast<long long*>(base + C::V_BYTES + C::HS_OR_STAGE + C::U_BYTES);
+  float* Us2 = reinterpret_cast<float*>(base + C::V_BYTES + C::HS_OR_STAGE);  // NUB x U_BYTES
+  long long* sinfo = reinterpret_cast<long long*>(base + C::V_BYTES + C::HS_OR_STAGE + C::NUB * C::U_BYTES);
+  uint64_t* ubar =
+      reinterpret_cast<uint64_t*>(base + C::V_BYTES + C::HS_OR_STAGE + C::NUB * C::U_BYTES + C::INFO_BYTES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cw_ = warp / C::SPL, part = warp - cw_ * C::SPL;
   const long long plane = (long long)P * g.cout_pad * g.cin_pad;  // hi -> lo (bf16 elements)
+  // prepped U: channel group k of the CTA's sequence (k = local chunk * groups + group) goes to
+  // buffer k & 1 by a bulk copy issued one group ahead, so staging U overlaps the previous group
+  const int ngroups = (g.cout_e + C::CO - 1) / C::CO;
+  const int nloc = (nchunks - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // chunks of this CTA
+  const long long nseq = (long long)nloc * ngroups;
+  constexpr int NUB = C::NUB;
+  auto u_issue = [&](long long k) {
+    if (k >= nseq) return;
+    const int grp = (int)(k % ngroups), b = (int)(k % NUB);
+    const uint32_t bar = ptx::smem_u32(&ubar[b]);
+    ptx::mbar_expect_tx(bar, (uint32_t)C::U_BYTES);
+    ptx::bulk_g2s(ptx::smem_u32(Us2 + b * (C::U_BYTES / 4)), Uc + (long long)grp * (C::U_BYTES / 4),
+                  (uint32_t)C::U_BYTES, bar);
+  };
+  if (Uc) {
+    if (tid == 0) {
+      for (int b = 0; b < NUB; ++b) ptx::mbar_init(ptx::smem_u32(&ubar[b]), 1);
+      ptx::mbar_init_fence();
+      if (NUB == 2) u_issue(0);
+    }
+    __syncthreads();
+  }
+  long long useq = 0;
 
   for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
     const long long t0 = (long long)chunk * 32;
@@ -104,7 +162,15 @@ __global__ void __launch_bounds__(FusedC1Cfg<MO, RO, MI>::THREADS, 1)
     }
     __syncthreads();
     // ---- 2. output channels in groups of CO: rows of M = V (.) U on the fly ----
-    for (int co0 = 0; co0 < g.cout_e; co0 += C::CO) {
+    for (int co0 = 0; co0 < g.cout_e; co0 += C::CO, ++useq) {
+      float* Us = Us2 + (Uc ? (useq % NUB) * (C::U_BYTES / 4) : 0);
+      if (Uc) {
+        if (tid == 0) {  // (next) group's U into the free buffer (its readers passed the last barrier)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          u_issue(NUB == 2 ? useq + 1 : useq);
+        }
+        ptx::mbar_wait(ptx::smem_u32(&ubar[useq % NUB]), (uint32_t)((useq / NUB) & 1));
+      } else
       for (int i = tid; i < P * C::CO; i += C::THREADS) {
         const int cl = i % C::CO, xi = i / C::CO, co = co0 + cl;
         float u = 0.f;
@@ -119,7 +185,7 @@ __global__ void __launch_bounds__(FusedC1Cfg<MO, RO, MI>::THREADS, 1)
         }
         Us[(cl * PA + xi / PA) * C::RPU + xi % PA] = u;
       }
-      __syncthreads();
+      if (!Uc) __syncthreads();
       const int coe = co0 + cw_;
       float* yst = Hs + warp * O::YST;
       long long* info = sinfo + warp * 64;
@@ -148,27 +214,38 @@ __global__ void __launch_bounds__(FusedC1Cfg<MO, RO, MI>::THREADS, 1)
 
 template <int MO, int RO, int MI, typename XT, typename YT>
 static nw_status_t fused_c1_launch(const nw_plan_st* p, const Geometry& g, const void* x, const void* U, void* y,
-                                   cudaStream_t s) {
+                                   void* ws, cudaStream_t s) {
   using C = FusedC1Cfg<MO, RO, MI>;
   static_assert(C::SMEM <= 227 * 1024, "fused single-channel kernel exceeds shared memory");
   if (ensure_smem<fused_c1_kernel<MO, RO, MI, XT, YT>>((int)C::SMEM) != NW_OK) return NW_ERR_CUDA;
+  const int umode = p->math == NW_MATH_FP32_SIMT ? 0 : (p->math == NW_MATH_BF16 ? 2 : 1);
+  float* Uc = static_cast<float*>(ws);
+  if (Uc) {  // per-group fp32 copy of U (workspace), bulk-copied by the kernel
+    const int ngroups = (g.cout_e + C::CO - 1) / C::CO;
+    const long long n = (long long)ngroups * C::CO * X_PA<MO, RO, MI>() * C::RPU;
+    LaunchScope scope_("fused_c1_prep", s);
+    fused_c1_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(U, umode, Uc, X_PA<MO, RO, MI>(), C::RPU, C::CO,
+                                                                     ngroups, g.cout_e, g.cout_pad, g.cin_pad);
+    nw_status_t st = check_launch();
+    if (st != NW_OK) return st;
+  }
   const long long nchunks = (g.T + 31) / 32;
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(nchunks < sms ? nchunks : sms);
   LaunchScope scope_("fused_c1", s);
   fused_c1_kernel<MO, RO, MI, XT, YT><<<grid, C::THREADS, C::SMEM, s>>>(
-      static_cast<const XT*>(x), U, p->math == NW_MATH_FP32_SIMT ? 0 : (p->math == NW_MATH_BF16 ? 2 : 1), static_cast<YT*>(y), g,
-      p->prelu ? p->slopes : nullptr, (int)nchunks);
+      static_cast<const XT*>(x), U, Uc, umode, static_cast<YT*>(y), g, p->prelu ? p->slopes : nullptr, (int)nchunks);
   return check_launch();
 }
 
 template <int MO, int RO, int MI>
-nw_status_t fused_c1_impl(const nw_plan_st* p, const Geometry& g, const void* x, const void* U, void* y,
+nw_status_t fused_c1_impl(const nw_plan_st* p, const Geometry& g, const void* x, const void* U, void* y, void* ws,
                           cudaStream_t s) {
   if constexpr (MI == 3 && Ax<MO, RO, MI>::NPH == 1 && Ax<MO, RO, MI>::PA <= 30) {
-    if (p->dtype == NW_DTYPE_BF16) return fused_c1_launch<MO, RO, MI, __nv_bfloat16, __nv_bfloat16>(p, g, x, U, y, s);
-    return fused_c1_launch<MO, RO, MI, float, float>(p, g, x, U, y, s);
+    if (p->dtype == NW_DTYPE_BF16)
+      return fused_c1_launch<MO, RO, MI, __nv_bfloat16, __nv_bfloat16>(p, g, x, U, y, ws, s);
+    return fused_c1_launch<MO, RO, MI, float, float>(p, g, x, U, y, ws, s);
   }
   return NW_ERR_UNSUPPORTED;
 }

@@ -79,6 +79,48 @@ __global__ void fused_co_prep_kernel(const void* __restrict__ U, int umode, floa
   U4[i] = make_float4(u[0], u[1], u[2], u[3]);
 }
 
+// The P_a x 4 channel-sum accumulators of one (slice, p_h) row.  Packed (PK): output lanes
+// (0, 1) and (2, 3) in f32x2 pairs, two FFMA2 (the V value as a broadcast scalar operand) per
+// V value instead of four FFMA, same per-lane rounding.  Measured 4 % SLOWER on C5's
+// deconvolution (1.37 -> 1.42 ms) and Table I's SRCNN 5x5 1 <- 32 (0.123 -> 0.128 ms): the
+// aligned register pairs cost moves and the kernel is not issue-bound there; so the scalar form
+// runs (the packed one stays for the record, and spills at P_a = 30 under 10 warps' 168-register
+// cap).
+template <int PA, bool PK>
+struct CoAcc {
+  float a[PA][4];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int p = 0; p < PA; ++p)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) a[p][k] = 0.f;
+  }
+  __device__ __forceinline__ void fma(int p, float v, const float4& u) {
+    a[p][0] = fmaf(v, u.x, a[p][0]);
+    a[p][1] = fmaf(v, u.y, a[p][1]);
+    a[p][2] = fmaf(v, u.z, a[p][2]);
+    a[p][3] = fmaf(v, u.w, a[p][3]);
+  }
+  __device__ __forceinline__ float get(int p, int co) const { return a[p][co]; }
+};
+template <int PA>
+struct CoAcc<PA, true> {
+  f2 a01[PA], a23[PA];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int p = 0; p < PA; ++p) a01[p] = a23[p] = f2_splat(0.f);
+  }
+  __device__ __forceinline__ void fma(int p, float v, const float4& u) {
+    a01[p] = fmaf(v, f2_pack(u.x, u.y), a01[p]);
+    a23[p] = fmaf(v, f2_pack(u.z, u.w), a23[p]);
+  }
+  __device__ __forceinline__ float get(int p, int co) const {
+    float x0, x1;
+    f2_unpack(co < 2 ? a01[p] : a23[p], x0, x1);
+    return (co & 1) ? x1 : x0;
+  }
+};
+
 template <int MO, int RO, int MI, typename XT, typename YT>
 __global__ void __launch_bounds__(FusedCoCfg<MO, RO, MI>::THREADS, 1)
     fused_co_kernel(const __grid_constant__ CUtensorMap mapX, const float4* __restrict__ U4, YT* __restrict__ y,
@@ -144,22 +186,47 @@ __global__ void __launch_bounds__(FusedCoCfg<MO, RO, MI>::THREADS, 1)
       ptx::mbar_wait(ptx::smem_u32(&full[st]), (uint32_t)((q / NSTG) & 1));
       const XT* win = reinterpret_cast<const XT*>(wring + st * WST) + sh;
       float* Hs = Hbuf + b * C::HS;
-      for (int task = tid; task < S * L; task += C::THREADS) {
-        const int s = task / L, col = task - (task / L) * L;
-        float xin[L], hv[PA];
-        const XT* src = win + s * X::ADV + col;
+      // two window columns per thread (FADD2 / FFMA2) spill: the P_a x 4 accumulators are live
+      // across pass 1 of the next channel, so pass 1 stays scalar here
+      if constexpr (false && kPackedAxis<MO, RO, MI>) {
+        for (int task = tid; task < S * L; task += 2 * C::THREADS) {
+          const int s = task / L, col = task - (task / L) * L;
+          const XT* src = win + s * X::ADV + col;
+          const int tb = task + C::THREADS;
+          if (tb < S * L) {
+            const int sb = tb / L, colb = tb - (tb / L) * L;
+            const XT* srcb = win + sb * X::ADV + colb;
+            f2 xin[L], hv[PA];
 #pragma unroll
-        for (int r = 0; r < L; ++r) xin[r] = to_f(src[r * BW]);
-        in_axis<MO, RO, MI>(xin, hv);
+            for (int r = 0; r < L; ++r) xin[r] = f2_pack(to_f(src[r * BW]), to_f(srcb[r * BW]));
+            in_axis_t<MO, RO, MI, f2>(xin, hv);
 #pragma unroll
-        for (int p = 0; p < PA; ++p) Hs[(s * PA + p) * C::HSTR + col] = hv[p];
+            for (int p = 0; p < PA; ++p)
+              f2_unpack(hv[p], Hs[(s * PA + p) * C::HSTR + col], Hs[(sb * PA + p) * C::HSTR + colb]);
+          } else {
+            float xin[L], hv[PA];
+#pragma unroll
+            for (int r = 0; r < L; ++r) xin[r] = to_f(src[r * BW]);
+            in_axis<MO, RO, MI>(xin, hv);
+#pragma unroll
+            for (int p = 0; p < PA; ++p) Hs[(s * PA + p) * C::HSTR + col] = hv[p];
+          }
+        }
+      } else {
+        for (int task = tid; task < S * L; task += C::THREADS) {
+          const int s = task / L, col = task - (task / L) * L;
+          float xin[L], hv[PA];
+          const XT* src = win + s * X::ADV + col;
+#pragma unroll
+          for (int r = 0; r < L; ++r) xin[r] = to_f(src[r * BW]);
+          in_axis<MO, RO, MI>(xin, hv);
+#pragma unroll
+          for (int p = 0; p < PA; ++p) Hs[(s * PA + p) * C::HSTR + col] = hv[p];
+        }
       }
     };
-    float acc[PA][CO];
-#pragma unroll
-    for (int p = 0; p < PA; ++p)
-#pragma unroll
-      for (int co = 0; co < CO; ++co) acc[p][co] = 0.f;
+    CoAcc<PA, false> acc;
+    acc.zero();
     pass1(q0, 0);
     __syncthreads();
     for (int c = 0; c < cin; ++c) {
@@ -174,11 +241,7 @@ __global__ void __launch_bounds__(FusedCoCfg<MO, RO, MI>::THREADS, 1)
         const float4* u = Us + (q % NSTG) * P + ph2 * PA;
 #pragma unroll
         for (int pw = 0; pw < PA; ++pw) {
-          const float4 uu = u[pw];
-          acc[pw][0] = fmaf(v[pw], uu.x, acc[pw][0]);
-          acc[pw][1] = fmaf(v[pw], uu.y, acc[pw][1]);
-          acc[pw][2] = fmaf(v[pw], uu.z, acc[pw][2]);
-          acc[pw][3] = fmaf(v[pw], uu.w, acc[pw][3]);
+          acc.fma(pw, v[pw], u[pw]);
         }
       }
       if (c + 1 < cin) pass1(q + 1, b ^ 1);
@@ -196,7 +259,7 @@ __global__ void __launch_bounds__(FusedCoCfg<MO, RO, MI>::THREADS, 1)
         if (co < g.cout_e) {
           float m[PA], yq[MA];
 #pragma unroll
-          for (int p = 0; p < PA; ++p) m[p] = acc[p][co];
+          for (int p = 0; p < PA; ++p) m[p] = acc.get(p, co);
           out_axis<MO, RO, MI>(m, yq);
           float* qd = Q + ((s2 * CO + co) * PA + ph2) * C::QSTR;
 #pragma unroll

@@ -129,8 +129,11 @@ nw_status_t launch_fused_co(const nw_plan_st *p, const Geometry &g, const void *
                             cudaStream_t s);
 // single-input-channel layers: the whole nested pipeline in one kernel (fused_small.cuh)
 bool fused_c1_eligible(const nw_plan_st *p, const Geometry &g);
+// ws (>= fused_c1_ws_bytes, or nullptr) receives the per-channel-group fp32 copy of U that the
+// kernel bulk-copies into shared memory
 nw_status_t launch_fused_c1(const nw_plan_st *p, const Geometry &g, const void *x, const void *U, void *y,
-                            cudaStream_t s);
+                            void *ws, size_t ws_bytes, cudaStream_t s);
+size_t fused_c1_ws_bytes(const nw_plan_st *p, const Geometry &g);
 
 // Launch with programmatic stream serialization (PDL): the kernel may start while the
 // previous kernel in the stream drains; it calls griddepcontrol.wait before reading
