@@ -36,7 +36,13 @@ struct InCfg {
   static constexpr int NPAIR = CC * SR * SR / 2;                // ce pairs per block
   static constexpr int PROWS = X::SHMAX + X::L;                 // window rows of one stride phase
   static constexpr int HS = X::NPH * X::PA * CC * CSTR;         // floats (one row phase at a time)
-  static constexpr size_t SMEM = (size_t)HS * sizeof(float);
+  // stride 2 with 8-channel CTAs (layers with <= 8 source channels, C4a): both row phases' Hs are
+  // kept, so pass 2 writes all 4 x cs phase-major contraction channels of a V row at once (full
+  // 32-byte sectors; one phase at a time left every sector half written across pass 1 of the
+  // other phase, and the L2 re-read the half-written sectors from DRAM: 540 MB of DRAM reads for a
+  // 154 MB input, profiles/r2x)
+  static constexpr bool BOTH = (SR == 2 && CC == 8);
+  static constexpr size_t SMEM = (size_t)HS * (BOTH ? 2 : 1) * sizeof(float);
   static constexpr int THREADS = (CC >= 64) ? 512 : (CC >= 32 || SR == 2) ? 256 : 128;
   static constexpr int MINB = 512 / THREADS;                    // resident CTAs per SM (registers <= 128)
 };
@@ -166,7 +172,8 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
   // other through the same shared buffer (half the footprint, twice the resident CTAs)
 #pragma unroll 1
   for (int p = 0; p < SR; ++p) {
-  if (p) __syncthreads();  // pass 2 of the previous phase is done with Hs
+  if (p && !C::BOTH) __syncthreads();  // pass 2 of the previous phase is done with Hs
+  float* Hp = Hs + (C::BOTH ? p * C::HS : 0);  // this row phase's pass-1 buffer
   // ---------------- pass 1: columns along h (straight from x) ----------------
   // every load of the thread's NT1 columns is issued before the first transform, so a CTA
   // waits for one global round trip per row phase instead of one per column (C2 and, since
@@ -218,7 +225,7 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
 #pragma unroll
       for (int r = 0; r < L; ++r) xin[r] = xr[i][sh + r];
       in_axis<MO, RO, MI>(xin, hv);
-      float* dst = Hs + (ph * PA * CC + c) * C::CSTR + col;
+      float* dst = Hp + (ph * PA * CC + c) * C::CSTR + col;
 #pragma unroll
       for (int q = 0; q < PA; ++q) dst[q * CC * C::CSTR] = hv[q];
     }
@@ -248,17 +255,20 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
 #pragma unroll
         for (int r = 0; r < L; ++r) xin[r] = xc[sh + r];
         in_axis<MO, RO, MI>(xin, hv);
-        float* dst = Hs + (ph * PA * CC + c) * C::CSTR + col;
+        float* dst = Hp + (ph * PA * CC + c) * C::CSTR + col;
 #pragma unroll
         for (int q = 0; q < PA; ++q) dst[q * CC * C::CSTR] = hv[q];
       }
     }
   }
+  if (C::BOTH && p + 1 < SR) continue;  // pass 2 once, after both row phases' pass 1
   __syncthreads();
 
   // ---------------- pass 2: rows along w, split, store V ----------------
-  // channel pairs; stride 2: pairs of each column phase q (phase-major ce = (2p + q) * cs + ci)
-  constexpr int NPR = (SR == 1) ? CC / 2 : CC;
+  // channel pairs; stride 2: pairs of each column phase q (phase-major ce = (2p + q) * cs + ci);
+  // BOTH: pairs of both row phases, (p, q, channel pair) with the pair fastest, so consecutive
+  // lanes write consecutive bytes of a V row
+  constexpr int NPR = (SR == 1) ? CC / 2 : (C::BOTH ? 2 * CC : CC);
   constexpr int NTASK = NPH * NPH * PA * C::TW * NPR;
 #pragma unroll 1
   for (int task = tid; task < NTASK; task += C::THREADS) {
@@ -272,17 +282,19 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
     const int pw = r % NPH;
     const int phh = r / NPH;
     const int aw = aw0 + tile;
-    int c0, c1, q0, q1, ce;
+    int c0, c1, q0, q1, ce, hoff = 0;
     if (SR == 1) {
       c0 = 2 * pr; c1 = c0 + 1; q0 = q1 = 0;
       ce = cin0 + c0;
     } else {
-      const int q = pr / (CC / 2), cp = pr - q * (CC / 2);
+      const int pb = C::BOTH ? pr / CC : p, prr = C::BOTH ? pr % CC : pr;
+      const int q = prr / (CC / 2), cp = prr - q * (CC / 2);
       c0 = 2 * cp; c1 = c0 + 1; q0 = q1 = q;
-      ce = (p * 2 + q) * g.cs + cin0 + c0;
+      ce = (pb * 2 + q) * g.cs + cin0 + c0;
+      hoff = C::BOTH ? pb * C::HS : 0;  // row phase pb's pass-1 buffer
     }
-    const float* h0 = Hs + ((phh * PA + p_h) * CC + c0) * C::CSTR;
-    const float* h1 = Hs + ((phh * PA + p_h) * CC + c1) * C::CSTR;
+    const float* h0 = Hs + hoff + ((phh * PA + p_h) * CC + c0) * C::CSTR;
+    const float* h1 = Hs + hoff + ((phh * PA + p_h) * CC + c1) * C::CSTR;
     const int cb = tile * X::ADV + (pw == 0 ? 0 : SH1);
     if (aw >= g.tiles_w || ce >= g.cin_pad || (SR == 2 && cin0 + c0 >= g.cs)) continue;
     float za[X::LO][X::LI], zb[X::LO][X::LI];
