@@ -137,7 +137,10 @@ __global__ void __launch_bounds__(FusedCoCfg<MO, RO, MI>::THREADS, 1)
   float* Hbuf = reinterpret_cast<float*>(base + NSTG * (WST + C::U_STAGE));  // 2 x HS, later Q
   uint64_t* full = reinterpret_cast<uint64_t*>(base + NSTG * (WST + C::U_STAGE) + C::BUF_BYTES);
   const int tid = threadIdx.x;
-  const int s2 = tid / PA, ph2 = tid - (tid / PA) * PA;  // pass-2 / w-output role: (slice, p_h)
+  // pass-2 / w-output role: (slice, p_h), slice fastest, so the 32 lanes of a warp share two or
+  // three point rows p_h and their U_c row loads (LDS.128 per point) are broadcasts; with p_h
+  // fastest every lane read its own U row (~0.5 ms of shared-memory wavefronts per C5 layer)
+  const int ph2 = tid / S, s2 = tid - (tid / S) * S;
   const bool row_thread = tid < C::ROWS;
   const int cin = g.cin_e;
 
