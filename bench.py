@@ -626,15 +626,16 @@ def main():
                                                outer_taps=l.r_o, output_padding=l.output_padding,
                                                prelu_slopes=conv.prelu_slopes)
                     conv.workspace(x.shape[0], x.shape[2], x.shape[3], path)
-                    conv(x, y, path=path)
+                    for _ in range(3):   # warm-up (first-use allocations, clocks)
+                        conv(x, y, path=path)
                     torch.cuda.synchronize()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record()
-                    for _ in range(3):
+                    for _ in range(10):
                         conv(x, y, path=path)
                     e1.record()
                     torch.cuda.synchronize()
-                    lm = e0.elapsed_time(e1) / 3
+                    lm = e0.elapsed_time(e1) / 10
                     tot += lm
                     lmath_name = "bf16" if lmath is not None else args.math
                     b = layer_bounds(l, conv.info, lmath_name, peaks, path)

@@ -1,11 +1,7 @@
+#!/bin/bash
+# GPU test suite + default bench line (quick check of a build): bash tools/gpu_check.sh
 mkdir -p gpurun_out
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 600 python -m pytest tests -m gpu -x -q -k "fp32_simt or lib_loaded or mixed or determin" > gpurun_out/pt_fp32.log 2>&1; echo "fp32 rc=$?"
-tail -5 gpurun_out/pt_fp32.log
-timeout 600 python -m pytest tests -m gpu -q > gpurun_out/pt_all.log 2>&1; echo "all rc=$?"
-tail -30 gpurun_out/pt_all.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
-tail -5 gpurun_out/smoke.log
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu > gpurun_out/bench_c2.log 2>&1; echo "bench rc=$?"
-tail -c 3000 gpurun_out/bench_c2.log
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/check_pt.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/check_pt.log
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/check_bench.json 2> gpurun_out/check_bench.err; echo "bench rc=$?"
+python -c "
+import json;d=json.load(open('gpurun_out/check_bench.json'));print(d['value'],d['ms_per_step'],d.get('graph'),d['roofline']['frac'],d['roofline']['avg_launch_ms']); print([(p['layer'],p['ms']) for p in d['per_layer']]); print(d['e2e'])"
