@@ -42,6 +42,9 @@ struct InCfg {
   // other phase, and the L2 re-read the half-written sectors from DRAM: 540 MB of DRAM reads for a
   // 154 MB input, profiles/r2x)
   static constexpr bool BOTH = (SR == 2 && CC == 8);
+  // other stride-2 CTAs take one row phase each (twice the CTAs, half the work each): the two
+  // phases' window loads are then in flight at once instead of one after the other's pass 2
+  static constexpr bool SPLITP = (SR == 2 && !BOTH);
   static constexpr size_t SMEM = (size_t)HS * (BOTH ? 2 : 1) * sizeof(float);
   static constexpr int THREADS = (CC >= 64) ? 512 : (CC >= 32 || SR == 2) ? 256 : 128;
   static constexpr int MINB = 512 / THREADS;                    // resident CTAs per SM (registers <= 128)
@@ -153,6 +156,8 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
   const int tid = threadIdx.x;
 
   int b = blockIdx.x;
+  const int pidx = C::SPLITP ? b % 2 : 0;  // SPLITP: this CTA's row phase
+  if (C::SPLITP) b /= 2;
   const int cg = b % cgroups;
   b /= cgroups;
   const int wg = b % wgroups;
@@ -171,8 +176,8 @@ __global__ void __launch_bounds__(InCfg<MO, RO, MI, SR, CC>::THREADS, InCfg<MO, 
   // stride 2: the two row phases p of the polyphase split (Eq. 2.7) run one after the
   // other through the same shared buffer (half the footprint, twice the resident CTAs)
 #pragma unroll 1
-  for (int p = 0; p < SR; ++p) {
-  if (p && !C::BOTH) __syncthreads();  // pass 2 of the previous phase is done with Hs
+  for (int p = pidx; p < (C::SPLITP ? pidx + 1 : SR); ++p) {
+  if (p > pidx && !C::BOTH) __syncthreads();  // pass 2 of the previous phase is done with Hs
   float* Hp = Hs + (C::BOTH ? p * C::HS : 0);  // this row phase's pass-1 buffer
   // ---------------- pass 1: columns along h (straight from x) ----------------
   // every load of the thread's NT1 columns is issued before the first transform, so a CTA
@@ -336,7 +341,7 @@ static nw_status_t input_launch_c(const Geometry& g, const void* x, void* V, cud
   const int wgroups = (g.tiles_w + C::TW - 1) / C::TW;
   const int cin_src = (SR == 1) ? g.cin_pad : g.cs;
   const int cgroups = (cin_src + CC - 1) / CC;
-  const long long nb = (long long)g.N * g.tiles_h * wgroups * cgroups;
+  const long long nb = (long long)g.N * g.tiles_h * wgroups * cgroups * (C::SPLITP ? 2 : 1);
   if (nb >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
   LaunchScope scope_("input_transform", s);
   if (launch_pdl(kern, dim3((unsigned)nb), dim3(C::THREADS), C::SMEM, s, static_cast<const XT*>(x), V, g, cgroups,
