@@ -169,9 +169,12 @@ static nw_status_t forward_one(const nw_plan_st *p, const Geometry &g, const voi
   if (si != sg) {
     if (cudaEventRecord(e_in, si) != cudaSuccess || cudaStreamWaitEvent(sg, e_in, 0) != cudaSuccess) return NW_ERR_CUDA;
   }
-  const bool fused = gemm_fused_eligible(p, g);  // inner output level in the contraction epilogue
+  const int flevel = gemm_fused_level(p, g);  // inner output level(s) in the contraction epilogue
+  const bool fused = flevel > 0;
   if (p->math == NW_MATH_FP32_SIMT)
     st = launch_gemm_simt(p, g, static_cast<const float *>(V), static_cast<const float *>(U), M, sg);
+  else if (flevel == 2)
+    st = launch_gemm_tc_fused2(p, g, V, U, M, sg);
   else if (fused)
     st = launch_gemm_tc_fused(p, g, V, U, M, sg);
   else
@@ -181,6 +184,7 @@ static nw_status_t forward_one(const nw_plan_st *p, const Geometry &g, const voi
     if (cudaEventRecord(e_gemm, sg) != cudaSuccess || cudaStreamWaitEvent(so, e_gemm, 0) != cudaSuccess)
       return NW_ERR_CUDA;
   }
+  if (flevel == 2) return launch_output_transform_pre2(p, g, M, y, so);
   return fused ? launch_output_transform_pre(p, g, M, y, so) : launch_output_transform(p, g, M, y, so);
 }
 

@@ -12,6 +12,8 @@ template <int MO, int RO, int MI>
 nw_status_t output_impl(const nw_plan_st*, const Geometry&, const float*, void*, cudaStream_t);
 template <int MO, int RO, int MI>
 nw_status_t output_impl_pre(const nw_plan_st*, const Geometry&, const float*, void*, cudaStream_t);
+template <int MO, int RO, int MI>
+nw_status_t output_impl_pre2(const nw_plan_st*, const Geometry&, const float*, void*, cudaStream_t);
 
 template <int MO, int RO, int MI>
 nw_status_t fused_c1_impl(const nw_plan_st*, const Geometry&, const void*, const void*, void*, void*, cudaStream_t);
@@ -44,6 +46,11 @@ nw_status_t launch_output_transform(const nw_plan_st* p, const Geometry& g, cons
 nw_status_t launch_output_transform_pre(const nw_plan_st* p, const Geometry& g, const float* M, void* y,
                                         cudaStream_t s) {
   NW_DISPATCH_AXIS(p, output_impl_pre, p, g, M, y, s);
+}
+
+nw_status_t launch_output_transform_pre2(const nw_plan_st* p, const Geometry& g, const float* M, void* y,
+                                         cudaStream_t s) {
+  NW_DISPATCH_AXIS(p, output_impl_pre2, p, g, M, y, s);
 }
 
 bool fused_c1_eligible(const nw_plan_st* p, const Geometry& g) {

@@ -19,7 +19,7 @@ constexpr int X_PA() { return Ax<MO, RO, MI>::PA; }
 template <int MO, int RO, int MI, int CO_>
 struct FusedC1Shape {
   using X = Ax<MO, RO, MI>;
-  using O = OutCfg<MO, RO, MI, false>;
+  using O = OutCfg<MO, RO, MI, 0>;
   static constexpr int SPL = O::SPL;
   static constexpr int CO = CO_;                                // output channels per pass
   static constexpr int WARPS = CO * SPL;
@@ -75,11 +75,11 @@ static __global__ void fused_c1_prep_kernel(const void* __restrict__ U, int umod
 template <int MO, int RO, int MI>
 struct FusedC1Cfg
     : FusedC1Shape<MO, RO, MI,
-                   (OutCfg<MO, RO, MI, false>::SPL == 1)
+                   (OutCfg<MO, RO, MI, 0>::SPL == 1)
                        ? 12
-                       : (FusedC1Shape<MO, RO, MI, 16 / OutCfg<MO, RO, MI, false>::SPL>::SMEM <= 227 * 1024
-                              ? 16 / OutCfg<MO, RO, MI, false>::SPL
-                              : 12 / OutCfg<MO, RO, MI, false>::SPL)> {};
+                       : (FusedC1Shape<MO, RO, MI, 16 / OutCfg<MO, RO, MI, 0>::SPL>::SMEM <= 227 * 1024
+                              ? 16 / OutCfg<MO, RO, MI, 0>::SPL
+                              : 12 / OutCfg<MO, RO, MI, 0>::SPL)> {};
 
 template <int MO, int RO, int MI, typename XT, typename YT>
 __global__ void __launch_bounds__(FusedC1Cfg<MO, RO, MI>::THREADS, 1)
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(FusedC1Cfg<MO, RO, MI>::THREADS, 1)
                     YT* __restrict__ y, Geometry g, const float* __restrict__ slopes, int nchunks) {
   using X = Ax<MO, RO, MI>;
   using C = FusedC1Cfg<MO, RO, MI>;
-  using O = OutCfg<MO, RO, MI, false>;
+  using O = OutCfg<MO, RO, MI, 0>;
   constexpr int PA = X::PA, L = X::L, P = C::P;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((128u - (ptx::smem_u32(smem_raw) & 127u)) & 127u);
@@ -202,10 +202,10 @@ __global__ void __launch_bounds__(FusedC1Cfg<MO, RO, MI>::THREADS, 1)
         }
       };
       if constexpr (C::SPL == 1) {
-        out_unit<MO, RO, MI, YT, false, 0>(t0, coe, prod_row, yst, info, y, g, slopes);
+        out_unit<MO, RO, MI, YT, 0, 0>(t0, coe, prod_row, yst, info, y, g, slopes);
       } else {
-        if (part == 0) out_unit<MO, RO, MI, YT, false, 0>(t0, coe, prod_row, yst, info, y, g, slopes);
-        else out_unit<MO, RO, MI, YT, false, 1>(t0, coe, prod_row, yst, info, y, g, slopes);
+        if (part == 0) out_unit<MO, RO, MI, YT, 0, 0>(t0, coe, prod_row, yst, info, y, g, slopes);
+        else out_unit<MO, RO, MI, YT, 0, 1>(t0, coe, prod_row, yst, info, y, g, slopes);
       }
       __syncthreads();  // Us and the stage are rewritten by the next group
     }

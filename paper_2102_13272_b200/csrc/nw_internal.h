@@ -114,6 +114,13 @@ nw_status_t launch_gemm_simt(const nw_plan_st *p, const Geometry &g, const float
 bool gemm_fused_eligible(const nw_plan_st *p, const Geometry &g);
 nw_status_t launch_gemm_tc_fused(const nw_plan_st *p, const Geometry &g, const void *V, const void *U, float *Mp,
                                  cudaStream_t s);
+// fusion level of the contraction epilogue: 0 plain (M), 1 inner output level along w (M'),
+// 2 inner level along both axes (M'' = (m_i / l_i)^2 of M)
+int gemm_fused_level(const nw_plan_st *p, const Geometry &g);
+nw_status_t launch_gemm_tc_fused2(const nw_plan_st *p, const Geometry &g, const void *V, const void *U, float *Mpp,
+                                  cudaStream_t s);
+nw_status_t launch_output_transform_pre2(const nw_plan_st *p, const Geometry &g, const float *Mpp, void *y,
+                                         cudaStream_t s);
 // output transform of a fused contraction: M holds M' (inner w level applied)
 nw_status_t launch_output_transform_pre(const nw_plan_st *p, const Geometry &g, const float *Mp, void *y,
                                         cudaStream_t s);

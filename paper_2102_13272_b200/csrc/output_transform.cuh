@@ -25,12 +25,14 @@
 
 namespace nw {
 
-template <int MO, int RO, int MI, bool PRE = false>
+template <int MO, int RO, int MI, int PRE = 0>
 struct OutCfg {
   using X = Ax<MO, RO, MI>;
-  // PRE: M already carries the inner output level along w (fused contraction
-  // epilogue), so a point row holds l_o * m_i values instead of P_a
+  // PRE = 1: M already carries the inner output level along w (fused contraction
+  // epilogue), so a point row holds l_o * m_i values instead of P_a.  PRE = 2: the inner level
+  // is applied along h as well (M''), so a unit has l_o * m_i rows (p_oh, j_h) instead of P_a.
   static constexpr int RL = PRE ? X::LO * MI : X::PA;
+  static constexpr int NR = (PRE == 2) ? X::LO * MI : X::PA;   // rows per unit
   // Threads keep (part of) the M_a x M_a output tile in registers.  Up to 9 x 9
   // one thread owns the tile (SPL = 1); larger outer kernels split the output
   // columns by outer index t into SPL parts of TH outer outputs each.
@@ -102,7 +104,7 @@ __device__ __forceinline__ float csel(const float (&v)[kMaxL], int i) {
 // One unit = 32 slices (lanes) x one output channel coe, one column part: accumulates
 // Y = A^T_hat M A_hat from the point rows rowsrc(r, mv) delivers (r = p_o * l_i + p_i),
 // then stores the tile (keep mask, crop, depth-to-space, PReLU, cast).
-template <int MO, int RO, int MI, typename YT, bool PRE, int PART, typename RowSrc>
+template <int MO, int RO, int MI, typename YT, int PRE, int PART, typename RowSrc>
 __device__ __forceinline__ void out_unit(long long t0, int coe, RowSrc&& rowsrc, float* yst, long long* info,
                                          YT* __restrict__ y, const Geometry& g, const float* __restrict__ slopes) {
   using X = Ax<MO, RO, MI>;
@@ -132,10 +134,11 @@ __device__ __forceinline__ void out_unit(long long t0, int coe, RowSrc&& rowsrc,
       for (int s = 0; s < MI; ++s)
 #pragma unroll
         for (int j = 0; j < QW; ++j) uacc[s][j] = 0.f;
+      constexpr int NI = (PRE == 2) ? MI : LI;  // rows per outer point: (p_o, j_h) when the h level is done
 #pragma unroll
-      for (int p_i = 0; p_i < LI; ++p_i) {
+      for (int p_i = 0; p_i < NI; ++p_i) {
         float mv[RL], qv[QW];
-        rowsrc(p_o * LI + p_i, mv);
+        rowsrc(p_o * NI + p_i, mv);
         // inner level along w on every outer point (done by the contraction epilogue when PRE)
         float uw[LO][MI];
 #pragma unroll
@@ -175,6 +178,10 @@ __device__ __forceinline__ void out_unit(long long t0, int coe, RowSrc&& rowsrc,
             for (int k = 0; k < C::TH; ++k) qv[k * MI + s2] = (T0 + k < MO) ? o[(T0 + k < MO) ? T0 + k : 0] : 0.f;
           }
         }
+        if constexpr (PRE == 2) {
+#pragma unroll
+          for (int j = 0; j < QW; ++j) uacc[p_i][j] = qv[j];
+        } else {
 #pragma unroll
         for (int s = 0; s < MI; ++s) {
           const float a = F.AiT[s][p_i];
@@ -188,6 +195,7 @@ __device__ __forceinline__ void out_unit(long long t0, int coe, RowSrc&& rowsrc,
 #pragma unroll
             for (int j = 0; j < QW; ++j) uacc[s][j] = fmaf(a, qv[j], uacc[s][j]);
           }
+        }
         }
       }
 #pragma unroll
@@ -377,7 +385,7 @@ __device__ __forceinline__ void out_unit(long long t0, int coe, RowSrc&& rowsrc,
   }
 }
 
-template <int MO, int RO, int MI, typename YT, bool PRE, int PART>
+template <int MO, int RO, int MI, typename YT, int PRE, int PART>
 __device__ __forceinline__ void out_consume(const float* ring, uint64_t* full, uint64_t* empty, float* ystage,
                                             long long* sinfo, YT* __restrict__ y, const Geometry& g,
                                             const float* __restrict__ slopes, int nunits, int ngroups) {
@@ -406,7 +414,7 @@ __device__ __forceinline__ void out_consume(const float* ring, uint64_t* full, u
   }
 }
 
-template <int MO, int RO, int MI, typename YT, bool PRE>
+template <int MO, int RO, int MI, typename YT, int PRE>
 __global__ void __launch_bounds__(OutCfg<MO, RO, MI, PRE>::THREADS, 1)
     output_transform_kernel(const __grid_constant__ CUtensorMap mapM, YT* __restrict__ y, Geometry g,
                             const float* __restrict__ slopes, int nunits, int ngroups) {
@@ -449,7 +457,7 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI, PRE>::THREADS, 1)
         if (g.sync2) {  // units walk the slices in order: wait for the contraction's units of t0's block
           for (; waited < (t0 >> 7); ++waited) ptx::wait_count(g.sync2 + waited + 1, PA * LO);
         }
-        for (int r = 0; r < PA; ++r) {
+        for (int r = 0; r < C::NR; ++r) {
           ptx::mbar_wait(ptx::smem_u32(&empty[st]), ph ^ 1);
           const uint32_t fb = ptx::smem_u32(&full[st]);
           ptx::mbar_expect_tx(fb, C::STAGE * 4);
@@ -477,14 +485,14 @@ __global__ void __launch_bounds__(OutCfg<MO, RO, MI, PRE>::THREADS, 1)
   }
 }
 
-template <int MO, int RO, int MI, typename YT, bool PRE>
+template <int MO, int RO, int MI, typename YT, int PRE>
 static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const float* M, void* y, cudaStream_t s) {
   using C = OutCfg<MO, RO, MI, PRE>;
   using X = Ax<MO, RO, MI>;
   auto kern = output_transform_kernel<MO, RO, MI, YT, PRE>;
   if (ensure_smem<output_transform_kernel<MO, RO, MI, YT, PRE>>((int)C::SMEM) != NW_OK) return NW_ERR_CUDA;
   alignas(64) CUtensorMap map;
-  const uint64_t rows = PRE ? (uint64_t)X::PA * C::RL : (uint64_t)g.P;
+  const uint64_t rows = PRE ? (uint64_t)C::NR * C::RL : (uint64_t)g.P;
   const uint64_t dims[3] = {(uint64_t)g.T_pad, (uint64_t)g.cout_pad, rows};
   const uint64_t strides[2] = {(uint64_t)g.T_pad * 4, (uint64_t)g.T_pad * g.cout_pad * 4};
   const uint32_t box[3] = {(uint32_t)C::TS, (uint32_t)C::CO, (uint32_t)C::RL};
@@ -506,14 +514,22 @@ static nw_status_t output_launch(const nw_plan_st* p, const Geometry& g, const f
 
 template <int MO, int RO, int MI>
 nw_status_t output_impl(const nw_plan_st* p, const Geometry& g, const float* M, void* y, cudaStream_t s) {
-  if (p->dtype == NW_DTYPE_BF16) return output_launch<MO, RO, MI, __nv_bfloat16, false>(p, g, M, y, s);
-  return output_launch<MO, RO, MI, float, false>(p, g, M, y, s);
+  if (p->dtype == NW_DTYPE_BF16) return output_launch<MO, RO, MI, __nv_bfloat16, 0>(p, g, M, y, s);
+  return output_launch<MO, RO, MI, float, 0>(p, g, M, y, s);
 }
 template <int MO, int RO, int MI>
 nw_status_t output_impl_pre(const nw_plan_st* p, const Geometry& g, const float* M, void* y, cudaStream_t s) {
   if constexpr (MI == 3) {
-    if (p->dtype == NW_DTYPE_BF16) return output_launch<MO, RO, MI, __nv_bfloat16, true>(p, g, M, y, s);
-    return output_launch<MO, RO, MI, float, true>(p, g, M, y, s);
+    if (p->dtype == NW_DTYPE_BF16) return output_launch<MO, RO, MI, __nv_bfloat16, 1>(p, g, M, y, s);
+    return output_launch<MO, RO, MI, float, 1>(p, g, M, y, s);
+  }
+  return NW_ERR_UNSUPPORTED;
+}
+template <int MO, int RO, int MI>
+nw_status_t output_impl_pre2(const nw_plan_st* p, const Geometry& g, const float* M, void* y, cudaStream_t s) {
+  if constexpr (MI == 3) {
+    if (p->dtype == NW_DTYPE_BF16) return output_launch<MO, RO, MI, __nv_bfloat16, 2>(p, g, M, y, s);
+    return output_launch<MO, RO, MI, float, 2>(p, g, M, y, s);
   }
   return NW_ERR_UNSUPPORTED;
 }

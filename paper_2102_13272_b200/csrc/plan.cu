@@ -304,7 +304,9 @@ nw_status_t nw_plan_info(nw_plan_t p, nw_plan_info_t *info) {
     // a representative geometry: 16-byte x rows (the single-kernel paths load x by TMA)
     const int side = (int)round_up(3 * p->K + 16, 8);
     Geometry g = make_geometry(p, 1, side, side);
-    info->m_rows = gemm_fused_eligible(p, g) ? p->ax.Pa * p->ax.l_o * p->m_i : info->points;
+    const int fl = gemm_fused_level(p, g);
+    info->m_rows = fl == 2 ? (p->ax.l_o * p->m_i) * (p->ax.l_o * p->m_i)
+                           : (fl == 1 ? p->ax.Pa * p->ax.l_o * p->m_i : info->points);
     info->single_kernel = (fused_c1_eligible(p, g) || fused_co_eligible(p, g)) ? 1 : 0;
     if (info->single_kernel) info->m_rows = 0;
   }

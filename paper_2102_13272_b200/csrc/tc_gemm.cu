@@ -117,6 +117,38 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
 }
 
+// Lean MMA issue for the fused kernels: the issuing lane was the bottleneck (ncu: ~26 dependent
+// instructions per MMA rebuilding both descriptors, ~150 cycles per MMA).  A descriptor's upper
+// word is constant per launch and its lower word is the shared address >> 4, so a k-step is one
+// add per operand.
+__device__ __forceinline__ uint32_t swk_desc_hi(int kbk) {
+  const uint32_t layout = kbk == 64 ? 2u : (kbk == 32 ? 4u : 6u);
+  return (((16u * (uint32_t)kbk) >> 4) & 0x3FFFu) | (1u << 14) | (layout << 29);
+}
+__device__ __forceinline__ uint64_t mk_desc(uint32_t hi, uint32_t lo) { return ((uint64_t)hi << 32) | (uint64_t)lo; }
+// one k-block (KS k-steps of 16) of one point: alo / blo = (stage A / B address) >> 4, apl / bpl =
+// (plane bytes) >> 4; accumulate = 0 starts the accumulator
+template <int KS>
+__device__ __forceinline__ void issue_kblock(uint32_t acc, uint32_t alo, uint32_t blo, uint32_t apl, uint32_t bpl,
+                                             uint32_t dhi, uint32_t idesc, int lo, uint32_t accumulate) {
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    const uint64_t ah = mk_desc(dhi, alo + 2 * k), bh = mk_desc(dhi, blo + 2 * k);
+    umma_f16(acc, ah, bh, idesc, k == 0 ? accumulate : 1u);
+    if (lo) {
+      umma_f16(acc, ah, mk_desc(dhi, blo + bpl + 2 * k), idesc, 1u);
+      umma_f16(acc, mk_desc(dhi, alo + apl + 2 * k), bh, idesc, 1u);
+    }
+  }
+}
+__device__ __forceinline__ void issue_kblock_any(int kbk, uint32_t acc, uint32_t alo, uint32_t blo, uint32_t apl,
+                                                 uint32_t bpl, uint32_t dhi, uint32_t idesc, int lo,
+                                                 uint32_t accumulate) {
+  if (kbk == 64) issue_kblock<4>(acc, alo, blo, apl, bpl, dhi, idesc, lo, accumulate);
+  else if (kbk == 32) issue_kblock<2>(acc, alo, blo, apl, bpl, dhi, idesc, lo, accumulate);
+  else issue_kblock<1>(acc, alo, blo, apl, bpl, dhi, idesc, lo, accumulate);
+}
+
 struct Params {
   int P;            // transform points
   int nmb;          // 128-slice blocks per point (T_pad / 128)
@@ -403,7 +435,9 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
   uint64_t* s_full = bars + 2 * kMaxStages;
   uint64_t* s_empty = bars + 2 * kMaxStages + kSlots;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 2 * kSlots);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so the role branches and everything the
+  // MMA warp computes stay in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int units = p.nmb * p.PA * p.LO;
   const uint32_t tcols = (uint32_t)(kSlots * p.N) <= 32 ? 32u : (uint32_t)(kSlots * p.N);
 
@@ -468,8 +502,11 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ------------------------- MMA issuer ---------------------------
-      const uint32_t idesc = idesc_bf16(p.N);
+    // ------------------------- MMA issuer ---------------------------
+    // the whole warp walks the loop and waits (uniform control flow keeps the descriptors in
+    // uniform registers: no per-MMA register-to-uniform broadcasts); lane 0 issues
+    {
+      const uint32_t idesc = idesc_bf16(p.N), dhi = swk_desc_hi(p.kbk);
       int st = 0;
       uint32_t ph = 0;
       uint32_t sc = 0;
@@ -483,19 +520,16 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
             mbar_wait(smem_u32(&full[st]), ph);
             fence_after();
             const uint32_t asm_ = base + (uint32_t)st * stage, bsm = asm_ + a_bytes;
-#pragma unroll
-            for (int k = 0; k < p.kbk / 16; ++k) {
-              const uint64_t ah = swk_desc(asm_ + k * 32, p.kbk), bh = swk_desc(bsm + k * 32, p.kbk);
-              umma_f16(acc, ah, bh, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-              if (p.lo) {
-                umma_f16(acc, ah, swk_desc(bsm + b_plane + k * 32, p.kbk), idesc, 1u);
-                umma_f16(acc, swk_desc(asm_ + a_plane + k * 32, p.kbk), bh, idesc, 1u);
-              }
+            if (lane == 0) {
+              issue_kblock_any(p.kbk, acc, asm_ >> 4, bsm >> 4, a_plane >> 4, b_plane >> 4, dhi, idesc, p.lo,
+                               kb > 0 ? 1u : 0u);
+              umma_commit(smem_u32(&empty[st]));
             }
-            umma_commit(smem_u32(&empty[st]));
+            __syncwarp();
             if (++st == p.nst) { st = 0; ph ^= 1; }
           }
-          umma_commit(smem_u32(&s_full[slot]));
+          if (lane == 0) umma_commit(smem_u32(&s_full[slot]));
+          __syncwarp();
         }
       }
     }
@@ -564,6 +598,234 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
   }
   fence_before();
   __syncthreads();
+  fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tcols));
+}
+
+// ---------------------------------------------------------------------------
+// Contraction with the inner output level along BOTH axes fused into the epilogue
+// (round 2, NW_FUSE_AI=2): Y = A^T_hat M A_hat with A^T_hat = A_o^T (x) A_i^T, and the inner
+// factor acts on the l_i x l_i points (p_ih, p_iw) of one outer point (p_oh, p_ow), so
+//   M''[((p_oh * m_i + j_h) * l_o + p_ow) * m_i + j_w][co][t]
+//       = sum_{p_ih, p_iw} A_i^T[j_h][p_ih] A_i^T[j_w][p_iw] M[(p_oh, p_ih), (p_ow, p_iw)][co][t]
+// is (m_i / l_i)^2 = 9/25 of M (M' is 15/25).  A thread must hold the m_i^2 partial sums of
+// its columns across the unit's l_i^2 points, which the register file allows for 16 columns
+// per thread: a unit is (outer point pair, 128-slice block, 32-channel half); the two halves
+// of one (point pair, block) are consecutive units, i.e. run on two CTAs at the same time,
+// so the second read of the A tiles is an L2 hit.  Accumulators rotate through 16 TMEM
+// slots of 32 columns; the 8 epilogue warps (lane quarter x column half) fold each
+// committed slot with the compile-time products of A_i^T entries.
+// ---------------------------------------------------------------------------
+constexpr int kSlots2 = 16;
+constexpr int kN2 = 32;  // channels per unit
+
+struct Fused2Params {
+  int nmb, N, nhalf, KB, lo, nst;
+  int kbk;
+  int PA, LO;
+  long long T_pad;
+  long long a_lo_row, b_lo_row;
+  int P, vblk;
+  float* Mpp;
+};
+
+template <int MI, int CL>
+__global__ void __launch_bounds__(kFuseThreads, 1)
+    contraction_fused2_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapU,
+                              const Fused2Params p) {
+  constexpr int LI = MI + 2;
+  constexpr Kernel1D KI = make_kernel(MI, 3);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* sbase = smem_raw + (base - raw);
+  const uint32_t a_plane = kBM * p.kbk * 2, b_plane = (uint32_t)kN2 * p.kbk * 2;
+  const uint32_t a_bytes = a_plane * (p.lo ? 2 : 1), b_bytes = b_plane * (p.lo ? 2 : 1);
+  const uint32_t stage = a_bytes + b_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + (size_t)stage * p.nst);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kMaxStages;
+  uint64_t* s_full = bars + 2 * kMaxStages;
+  uint64_t* s_empty = bars + 2 * kMaxStages + kSlots2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 2 * kSlots2);
+  // warp index through a shuffle: provably warp-uniform, so the role branches and everything the
+  // MMA warp computes stay in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  // CL = 2: the two channel halves of a (point pair, block) run on the two CTAs of a cluster; each
+  // CTA loads 64 of the 128 rows of every A tile and multicasts them to both, so V is read from
+  // L2 once per pair (unpaired CTAs drifted apart and the second read came from HBM)
+  const int units = p.nmb * p.LO * p.LO * (CL > 1 ? 1 : p.nhalf);
+  const int rank = (CL > 1) ? (int)cluster_rank() : 0;
+  const int ustart = (int)blockIdx.x / CL, ustep = (int)gridDim.x / CL;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
+  constexpr uint32_t tcols = kSlots2 * kN2;  // 512
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapV);
+    tma_prefetch(&mapU);
+    for (int i = 0; i < p.nst; ++i) { mbar_init(smem_u32(&full[i]), 1); mbar_init(smem_u32(&empty[i]), CL); }
+    for (int i = 0; i < kSlots2; ++i) { mbar_init(smem_u32(&s_full[i]), 1); mbar_init(smem_u32(&s_empty[i]), 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(tcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+  }
+  fence_before();
+  __syncthreads();
+  if constexpr (CL > 1) cluster_sync();  // every CTA's barriers are initialised before multicasts target them
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_launch_dependents();
+  griddep_wait();  // V comes from the input transform just before in the stream
+
+  // unit u -> (outer point pair pg = p_oh * l_o + p_ow, block mb, channel half nh), half fastest
+  auto decode = [&](int u, int& pg, int& mb, int& nh) {
+    nh = (CL > 1) ? rank : u % p.nhalf;
+    const int r = (CL > 1) ? u : u / p.nhalf;
+    pg = r / p.nmb;
+    mb = r - pg * p.nmb;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------- TMA producer -------------------------
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = ustart; u < units; u += ustep) {
+        int pg, mb, nh;
+        decode(u, pg, mb, nh);
+        const int p_oh = pg / p.LO, p_ow = pg - p_oh * p.LO;
+        for (int pt = 0; pt < LI * LI; ++pt) {
+          const int pih = pt / LI, piw = pt - pih * LI;
+          const int xi = (p_oh * LI + pih) * p.PA + p_ow * LI + piw;
+          for (int kb = 0; kb < p.KB; ++kb) {
+            mbar_wait(smem_u32(&empty[st]), ph ^ 1);
+            const uint32_t fb = smem_u32(&full[st]);
+            mbar_expect_tx(fb, stage);
+            const uint32_t dst = base + (uint32_t)st * stage;
+            long long row, lrow;
+            if (p.vblk) {
+              row = ((long long)mb * p.P + xi) * (2 * kBM);
+              lrow = row + kBM;
+            } else {
+              row = (long long)xi * p.T_pad + (long long)mb * kBM;
+              lrow = p.a_lo_row + row;
+            }
+            if constexpr (CL > 1) {
+              const int hr = kBM / CL;  // this CTA's rows of the A tile, multicast to the pair
+              const uint32_t so = (uint32_t)(rank * hr) * (uint32_t)(p.kbk * 2);
+              tma_load_2d_mc(dst + so, &mapV, fb, kb * p.kbk, (int)row + rank * hr, kMask);
+              if (p.lo) tma_load_2d_mc(dst + a_plane + so, &mapV, fb, kb * p.kbk, (int)lrow + rank * hr, kMask);
+            } else {
+              tma_load_2d(dst, &mapV, fb, kb * p.kbk, (int)row);
+              if (p.lo) tma_load_2d(dst + a_plane, &mapV, fb, kb * p.kbk, (int)lrow);
+            }
+            const int brow = xi * p.N + nh * kN2;
+            tma_load_2d(dst + a_bytes, &mapU, fb, kb * p.kbk, brow);
+            if (p.lo) tma_load_2d(dst + a_bytes + b_plane, &mapU, fb, kb * p.kbk, (int)(p.b_lo_row + brow));
+            if (++st == p.nst) { st = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------- MMA issuer (warp-uniform loop, lane 0 issues) ---------------------------
+    {
+      const uint32_t idesc = idesc_bf16(kN2), dhi = swk_desc_hi(p.kbk);
+      int st = 0;
+      uint32_t ph = 0;
+      uint32_t sc = 0;
+      for (int u = ustart; u < units; u += ustep) {
+        for (int pt = 0; pt < LI * LI; ++pt, ++sc) {
+          const uint32_t slot = sc % kSlots2, spar = (sc / kSlots2) & 1;
+          mbar_wait(smem_u32(&s_empty[slot]), spar ^ 1);
+          fence_after();
+          const uint32_t acc = tmem_base + slot * (uint32_t)kN2;
+          for (int kb = 0; kb < p.KB; ++kb) {
+            mbar_wait(smem_u32(&full[st]), ph);
+            fence_after();
+            const uint32_t asm_ = base + (uint32_t)st * stage, bsm = asm_ + a_bytes;
+            if (lane == 0) {
+              issue_kblock_any(p.kbk, acc, asm_ >> 4, bsm >> 4, a_plane >> 4, b_plane >> 4, dhi, idesc, p.lo,
+                               kb > 0 ? 1u : 0u);
+              if constexpr (CL > 1) umma_commit_mc(smem_u32(&empty[st]), kMask);  // frees the stage in both CTAs
+              else umma_commit(smem_u32(&empty[st]));
+            }
+            __syncwarp();
+            if (++st == p.nst) { st = 0; ph ^= 1; }
+          }
+          if (lane == 0) umma_commit(smem_u32(&s_full[slot]));
+          __syncwarp();
+        }
+      }
+    }
+  } else {  // ------------------------------- epilogue ----------------------------------
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    uint32_t sc = 0;
+    for (int u = ustart; u < units; u += ustep) {
+      int pg, mb, nh;
+      decode(u, pg, mb, nh);
+      const int p_oh = pg / p.LO, p_ow = pg - p_oh * p.LO;
+      float out[MI][MI][16];
+#pragma unroll
+      for (int a = 0; a < MI; ++a)
+#pragma unroll
+        for (int b = 0; b < MI; ++b)
+#pragma unroll
+          for (int c = 0; c < 16; ++c) out[a][b][c] = 0.f;
+#pragma unroll
+      for (int pih = 0; pih < LI; ++pih) {
+#pragma unroll
+        for (int piw = 0; piw < LI; ++piw, ++sc) {
+          const uint32_t slot = sc % kSlots2, spar = (sc / kSlots2) & 1;
+          mbar_wait(smem_u32(&s_full[slot]), spar);
+          fence_after();
+          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * (uint32_t)kN2 + (uint32_t)(half * 16);
+          uint32_t r0[16];
+          tmem_ld16(taddr, r0);
+          tmem_ld_wait();
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&s_empty[slot]));
+#pragma unroll
+          for (int jh = 0; jh < MI; ++jh) {
+            const float ah = float(rdouble(KI.AT[jh][pih]));
+            if (ah == 0.f) continue;
+#pragma unroll
+            for (int jw = 0; jw < MI; ++jw) {
+              const float a = ah * float(rdouble(KI.AT[jw][piw]));
+              if (a == 0.f) continue;
+#pragma unroll
+              for (int c = 0; c < 16; ++c) out[jh][jw][c] = fmaf(a, __uint_as_float(r0[c]), out[jh][jw][c]);
+            }
+          }
+        }
+      }
+      const long long t = (long long)mb * kBM + q * 32 + lane;
+      const int col0 = nh * kN2 + half * 16;
+      const int rl = p.LO * MI;  // M'' values per row of the (p_oh, j_h) grid
+      const long long pitch = p.T_pad;
+#pragma unroll
+      for (int jh = 0; jh < MI; ++jh) {
+#pragma unroll
+        for (int jw = 0; jw < MI; ++jw) {
+          const long long R = (long long)(p_oh * MI + jh) * rl + p_ow * MI + jw;
+          float* dst = p.Mpp + (R * p.N + col0) * p.T_pad + t;
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            *dst = out[jh][jw][c];
+            long long w = pitch;
+            asm volatile("" : "+l"(w));  // keep the walk incremental (no hoisted per-store offsets)
+            dst += w;
+          }
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if constexpr (CL > 1) cluster_sync();  // no CTA leaves while its pair may still multicast into it
   fence_after();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tcols));
 }
@@ -690,14 +952,91 @@ nw_status_t launch_gemm_tc(const nw_plan_st* p, const Geometry& g, const void* V
 // Fused contraction + inner output level (see contraction_fused_kernel).  Eligible
 // for the nested path in the tensor-core modes with Cout_pad in {32, 64} and
 // inner F(3,3); M' ([P_a * l_o * m_i][cout_pad][T_pad]) is written to M.
-bool gemm_fused_eligible(const nw_plan_st* p, const Geometry& g) {
+static int fuse_ai_env() {  // NW_FUSE_AI: 0 off, 1 inner level along w, 2 along both axes (default)
   static const int on = [] {
     const char* v = getenv("NW_FUSE_AI");
-    return v ? atoi(v) : 1;
+    return v ? atoi(v) : 2;
   }();
-  return on && !p->depthwise && g.path == kPathNested && p->math != NW_MATH_FP32_SIMT &&
+  return on;
+}
+bool gemm_fused_eligible(const nw_plan_st* p, const Geometry& g) {
+  return fuse_ai_env() && !p->depthwise && g.path == kPathNested && p->math != NW_MATH_FP32_SIMT &&
          (g.cout_pad == 32 || g.cout_pad == 64) &&
          g.mi == 3 && g.nsh == 1;
+}
+// 0: plain contraction (M), 1: M' (inner level along w), 2: M'' (inner level along both axes;
+// stream-ordered launches only: the streamed pipeline's counters belong to level 1)
+int gemm_fused_level(const nw_plan_st* p, const Geometry& g) {
+  if (!gemm_fused_eligible(p, g)) return 0;
+  return (fuse_ai_env() >= 2 && !g.sync && !g.sync2) ? 2 : 1;
+}
+
+nw_status_t launch_gemm_tc_fused2(const nw_plan_st* p, const Geometry& g, const void* V, const void* U, float* Mpp,
+                                  cudaStream_t s) {
+  tc::Fused2Params prm{};
+  prm.nmb = (int)(g.T_pad / tc::kBM);
+  prm.N = g.cout_pad;
+  prm.nhalf = g.cout_pad / tc::kN2;
+  prm.kbk = pick_kbk(g.cin_pad);
+  prm.KB = (g.cin_pad + prm.kbk - 1) / prm.kbk;
+  prm.lo = (p->math == NW_MATH_BF16X3) ? 1 : 0;
+  const NestedAxis ax = path_axis(p, g.path);
+  prm.PA = ax.Pa;
+  prm.LO = ax.l_o;
+  prm.T_pad = g.T_pad;
+  prm.a_lo_row = (long long)g.P * g.T_pad;
+  prm.b_lo_row = (long long)g.P * g.cout_pad;
+  prm.P = g.P;
+  prm.vblk = (g.vblk && prm.lo) ? 1 : 0;
+  prm.Mpp = Mpp;
+  const uint32_t stage = (tc::kBM * prm.kbk * 2 + (uint32_t)tc::kN2 * prm.kbk * 2) * (prm.lo ? 2 : 1);
+  prm.nst = (int)((200u * 1024u) / stage);
+  if (prm.nst > tc::kMaxStages) prm.nst = tc::kMaxStages;
+  if (prm.nst < 2) return NW_ERR_UNSUPPORTED;
+  size_t smem = 1024 + (size_t)stage * prm.nst + (2 * tc::kMaxStages + 2 * tc::kSlots2 + 2) * 8;
+  if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM: each CTA owns all 512 TMEM columns
+  const long long rowsV = (long long)g.P * g.T_pad * (prm.lo ? 2 : 1);
+  const long long rowsU = (long long)g.P * g.cout_pad * (prm.lo ? 2 : 1);
+  if (rowsV >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
+  alignas(64) CUtensorMap mapV, mapU;
+  // CTA pairs (one channel half each, A multicast) when the layer has two halves; NW_CLUSTER=1 unpairs
+  static const int cl_env = [] {
+    const char* v = getenv("NW_CLUSTER");
+    return v ? atoi(v) : 2;
+  }();
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (g.gemm_ctas > 0 && g.gemm_ctas < sms) sms = g.gemm_ctas;
+  const int CL = (prm.nhalf == 2 && cl_env == 2 && sms >= 2) ? 2 : 1;
+  if (!make_map(&mapV, V, rowsV, g.cin_pad, tc::kBM / CL, prm.kbk)) return NW_ERR_CUDA;
+  if (!make_map(&mapU, U, rowsU, g.cin_pad, tc::kN2, prm.kbk)) return NW_ERR_CUDA;
+  if ((CL > 1 ? ensure_smem<tc::contraction_fused2_kernel<3, 2>>(227 * 1024)
+              : ensure_smem<tc::contraction_fused2_kernel<3, 1>>(227 * 1024)) != NW_OK)
+    return NW_ERR_CUDA;
+  const long long units = (long long)prm.nmb * prm.LO * prm.LO * prm.nhalf;  // CTA-units
+  int grid = (int)(units < sms ? units : sms);
+  if (grid > prm.nhalf) grid -= grid % prm.nhalf;  // the halves of a (point pair, block) stay on CTA pairs
+  LaunchScope scope_("contraction_tc", s);
+  if (CL > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tc::kFuseThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, tc::contraction_fused2_kernel<3, 2>, mapV, mapU, prm) != cudaSuccess)
+      return NW_ERR_CUDA;
+  } else if (launch_pdl(tc::contraction_fused2_kernel<3, 1>, dim3(grid), dim3(tc::kFuseThreads), smem, s, mapV, mapU,
+                        prm) != NW_OK) {
+    return NW_ERR_CUDA;
+  }
+  return check_launch();
 }
 
 nw_status_t launch_gemm_tc_fused(const nw_plan_st* p, const Geometry& g, const void* V, const void* U, float* Mp,
@@ -730,7 +1069,8 @@ nw_status_t launch_gemm_tc_fused(const nw_plan_st* p, const Geometry& g, const v
   prm.nst = (int)((200u * 1024u) / stage);
   if (prm.nst > tc::kMaxStages) prm.nst = tc::kMaxStages;
   if (prm.nst < 2) return NW_ERR_UNSUPPORTED;
-  const size_t smem = 1024 + (size_t)stage * prm.nst + (2 * tc::kMaxStages + 2 * tc::kSlots + 2) * 8;
+  size_t smem = 1024 + (size_t)stage * prm.nst + (2 * tc::kMaxStages + 2 * tc::kSlots + 2) * 8;
+  if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM (a second CTA would wait for TMEM columns)
   const long long rowsV = (long long)g.P * g.T_pad * (prm.lo ? 2 : 1);
   const long long rowsU = (long long)g.P * g.cout_pad * (prm.lo ? 2 : 1);
   if (rowsV >= (1ll << 31)) return NW_ERR_UNSUPPORTED;

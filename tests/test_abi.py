@@ -118,11 +118,12 @@ def test_comparison_workspace_geometry(K, pad):
 
 def test_m_rows_reports_fused_inner_output_level():
     # the contraction writes M (P_a^2 rows per slice) or, with the inner output level of A^T_hat
-    # fused into its epilogue, P_a * l_o * m_i rows (A^T_hat = A_o^T (x) A_i^T)
+    # fused into its epilogue along w, P_a * l_o * m_i rows, along both axes (l_o * m_i)^2 rows
+    # (A^T_hat = A_o^T (x) A_i^T)
     for K, m_o, C in ((9, 4, 64), (9, 3, 64), (9, 4, 256), (5, 3, 16)):
         inf = _lib.Plan(K, 1, m_o, 3, C, C).info()
         l_o = m_o + 2
-        assert inf["m_rows"] in (inf["points"], inf["points_axis"] * l_o * 3)
+        assert inf["m_rows"] in (inf["points"], inf["points_axis"] * l_o * 3, (l_o * 3) ** 2)
     assert _lib.Plan(9, 1, 4, 3, 64, 64, math=_lib.MATH_FP32_SIMT).info()["m_rows"] == 900
 
 

@@ -3,8 +3,8 @@ fresh process (the library reads them once) and compared with the default path.
 
 Tunables that only change scheduling (chunking, CTA pairs, K-block width, unit size,
 launch mode, channels per CTA) must give BIT-IDENTICAL outputs: every output is the
-same sequence of fp32 operations.  Tunables that change the arithmetic (NW_FUSE_AI=0:
-the inner output level leaves the contraction epilogue; NW_FUSED_C1=0: the three-kernel
+same sequence of fp32 operations.  Tunables that change the arithmetic (NW_FUSE_AI=0 / 1:
+the inner output level leaves the contraction epilogue / is applied along w only; NW_FUSED_C1=0: the three-kernel
 pipeline instead of the single fused kernel) are checked against the FP64 oracle with the
 BASELINE gate.  Also the bench's end-to-end configuration: nw_conv_forward_host at N = 32
 with NW_HOST_CHUNKS=4 (chunk schedule 1,2,4,8,8,4,2,1... with a short tail) bit for bit
@@ -85,19 +85,23 @@ BITWISE = [
 @pytest.mark.parametrize("spec,env", BITWISE, ids=[f"{s['config']}-{'-'.join(f'{k}={v}' for k, v in e.items())}"
                                                    for s, e in BITWISE])
 def test_scheduling_tunables_bit_identical(spec, env, tmp_path):
-    y0 = _run(dict(spec), None, tmp=tmp_path)
-    y1 = _run(dict(spec), env, tmp=tmp_path)
+    # the streamed pipeline's counters belong to the w-only fused contraction (NW_FUSE_AI=1)
+    base = {"NW_FUSE_AI": "1"} if "NW_STREAM" in env else None
+    y0 = _run(dict(spec), base, tmp=tmp_path)
+    y1 = _run(dict(spec), {**env, **(base or {})}, tmp=tmp_path)
     assert y0.shape == y1.shape
     assert np.array_equal(y0, y1), float(np.abs(y0 - y1).max())
 
 
 ARITH = [
     (C2, {"NW_FUSE_AI": "0"}),
+    (C2, {"NW_FUSE_AI": "1"}),      # inner output level along w only (default 2: both axes)
+    (C4B, {"NW_FUSE_AI": "1"}),
     ({"config": "c5_conv1", "N": 2, "H": 37, "W": 45}, {"NW_FUSED_C1": "0"}),
 ]
 
 
-@pytest.mark.parametrize("spec,env", ARITH, ids=["fuse_ai_off", "fused_c1_off"])
+@pytest.mark.parametrize("spec,env", ARITH, ids=["fuse_ai_off", "fuse_ai_w_c2", "fuse_ai_w_c4b", "fused_c1_off"])
 def test_arithmetic_tunables_meet_gate(spec, env, tmp_path):
     y = _run(dict(spec), env, tmp=tmp_path)
     s = dict(spec)
