@@ -61,6 +61,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+// one lane of a converged warp (elect.sync): ptxas knows exactly one thread is active inside the
+// branch, so single-thread instructions (tcgen05.mma / commit) need no per-instruction election loop
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t"
+      "}"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ---- cluster helpers (CTA pairs sharing the B operand) ----
@@ -520,7 +533,7 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
             mbar_wait(smem_u32(&full[st]), ph);
             fence_after();
             const uint32_t asm_ = base + (uint32_t)st * stage, bsm = asm_ + a_bytes;
-            if (lane == 0) {
+            if (elect_one()) {
               issue_kblock_any(p.kbk, acc, asm_ >> 4, bsm >> 4, a_plane >> 4, b_plane >> 4, dhi, idesc, p.lo,
                                kb > 0 ? 1u : 0u);
               umma_commit(smem_u32(&empty[st]));
@@ -528,7 +541,7 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
             __syncwarp();
             if (++st == p.nst) { st = 0; ph ^= 1; }
           }
-          if (lane == 0) umma_commit(smem_u32(&s_full[slot]));
+          if (elect_one()) umma_commit(smem_u32(&s_full[slot]));
           __syncwarp();
         }
       }
@@ -689,7 +702,7 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
   };
 
   if (warp == 0) {
-    if (lane == 0) {  // ------------------------- TMA producer -------------------------
+    {  // ------------------------- TMA producer (warp-uniform loop, one elected lane issues) -------------------------
       int st = 0;
       uint32_t ph = 0;
       for (int u = ustart; u < units; u += ustep) {
@@ -702,7 +715,6 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
           for (int kb = 0; kb < p.KB; ++kb) {
             mbar_wait(smem_u32(&empty[st]), ph ^ 1);
             const uint32_t fb = smem_u32(&full[st]);
-            mbar_expect_tx(fb, stage);
             const uint32_t dst = base + (uint32_t)st * stage;
             long long row, lrow;
             if (p.vblk) {
@@ -712,6 +724,8 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
               row = (long long)xi * p.T_pad + (long long)mb * kBM;
               lrow = p.a_lo_row + row;
             }
+            if (elect_one()) {
+            mbar_expect_tx(fb, stage);
             if constexpr (CL > 1) {
               const int hr = kBM / CL;  // this CTA's rows of the A tile, multicast to the pair
               const uint32_t so = (uint32_t)(rank * hr) * (uint32_t)(p.kbk * 2);
@@ -724,6 +738,8 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
             const int brow = xi * p.N + nh * kN2;
             tma_load_2d(dst + a_bytes, &mapU, fb, kb * p.kbk, brow);
             if (p.lo) tma_load_2d(dst + a_bytes + b_plane, &mapU, fb, kb * p.kbk, (int)(p.b_lo_row + brow));
+            }
+            __syncwarp();
             if (++st == p.nst) { st = 0; ph ^= 1; }
           }
         }
@@ -746,7 +762,7 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
             mbar_wait(smem_u32(&full[st]), ph);
             fence_after();
             const uint32_t asm_ = base + (uint32_t)st * stage, bsm = asm_ + a_bytes;
-            if (lane == 0) {
+            if (elect_one()) {
               issue_kblock_any(p.kbk, acc, asm_ >> 4, bsm >> 4, a_plane >> 4, b_plane >> 4, dhi, idesc, p.lo,
                                kb > 0 ? 1u : 0u);
               if constexpr (CL > 1) umma_commit_mc(smem_u32(&empty[st]), kMask);  // frees the stage in both CTAs
@@ -755,7 +771,7 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
             __syncwarp();
             if (++st == p.nst) { st = 0; ph ^= 1; }
           }
-          if (lane == 0) umma_commit(smem_u32(&s_full[slot]));
+          if (elect_one()) umma_commit(smem_u32(&s_full[slot]));
           __syncwarp();
         }
       }
