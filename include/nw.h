@@ -30,7 +30,8 @@
  *    workspace.
  *  - Environment tunables (performance only; results are bit-identical or within
  *    rounding order, never a different algorithm): NW_FUSE_AI=0 disables the
- *    inner output level in the contraction epilogue; NW_IN_CC=16|32|64 source
+ *    inner output level in the contraction epilogue, 1 applies it along w only (default 2:
+ *    along both axes); NW_IN_CC=16|32|64 source
  *    channels per input-transform CTA (default 32); NW_PIPE_CHUNKS=k runs
  *    nw_conv_forward as a k-chunk three-stream pipeline (default 1) and
  *    NW_GEMM_CTAS caps its contraction grid; NW_HOST_CHUNKS=k sets the chunk
@@ -131,8 +132,9 @@ typedef struct {
   int cin_pad, cout_pad; /* cin_e / cout_e rounded up to the tensor-core granule (16) */
   int math, dtype;
   size_t filter_bytes; /* bytes of U for nw_transform_filter */
-  int m_rows;          /* transform-domain rows per slice the contraction writes: points, or
-                          P_a * l_o * m_i when the inner output level is fused into its epilogue */
+  int m_rows;          /* transform-domain rows per slice the contraction writes: points, or, with the
+                          inner output level fused into its epilogue, P_a * l_o * m_i (along w only)
+                          or (l_o * m_i)^2 (along both axes, the default) */
   int single_kernel;   /* 1: nw_conv_forward runs the layer as ONE kernel -- one input channel (the
                           contraction is a pointwise product) or at most four contraction outputs
                           (Cout_e <= 4: the channel sum accumulates in registers, x rows of a

@@ -630,6 +630,11 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
 // committed slot with the compile-time products of A_i^T entries.
 // ---------------------------------------------------------------------------
 constexpr int kSlots2 = 16;
+constexpr int kMaxStages2 = 16;  // small-K layers (10 KB stages) need > 8 stages in flight to cover the load latency
+// warpgroup 0: warp 0 TMA, warp 1 MMA (2, 3 idle); warpgroups 1, 2: epilogue.  setmaxnreg moves
+// registers from warpgroup 0 to the epilogue warps, whose 144 partial sums + two slot buffers
+// exceed the 168 registers a 12-warp CTA starts with.
+constexpr int kFuse2Threads = 384;
 constexpr int kN2 = 32;  // channels per unit
 
 struct Fused2Params {
@@ -643,7 +648,7 @@ struct Fused2Params {
 };
 
 template <int MI, int CL>
-__global__ void __launch_bounds__(kFuseThreads, 1)
+__global__ void __launch_bounds__(kFuse2Threads, 1)
     contraction_fused2_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapU,
                               const Fused2Params p) {
   constexpr int LI = MI + 2;
@@ -657,10 +662,10 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
   const uint32_t stage = a_bytes + b_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + (size_t)stage * p.nst);
   uint64_t* full = bars;
-  uint64_t* empty = bars + kMaxStages;
-  uint64_t* s_full = bars + 2 * kMaxStages;
-  uint64_t* s_empty = bars + 2 * kMaxStages + kSlots2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 2 * kSlots2);
+  uint64_t* empty = bars + kMaxStages2;
+  uint64_t* s_full = bars + 2 * kMaxStages2;
+  uint64_t* s_empty = bars + 2 * kMaxStages2 + kSlots2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages2 + 2 * kSlots2);
   // warp index through a shuffle: provably warp-uniform, so the role branches and everything the
   // MMA warp computes stay in uniform registers
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -701,6 +706,8 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
     mb = r - pg * p.nmb;
   };
 
+  if (warp < 4) {  // warpgroup 0 gives registers away; its role code stays inside this branch
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
   if (warp == 0) {
     {  // ------------------------- TMA producer (warp-uniform loop, one elected lane issues) -------------------------
       int st = 0;
@@ -776,8 +783,10 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
         }
       }
     }
-  } else {  // ------------------------------- epilogue ----------------------------------
-    const int q = warp & 3, half = (warp - 2) >> 2;
+  }
+  } else {  // ------------------------------- epilogue (warpgroups 1 and 2) ----------------------------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+    const int q = warp & 3, half = (warp - 4) >> 2;
     uint32_t sc = 0;
     for (int u = ustart; u < units; u += ustep) {
       int pg, mb, nh;
@@ -790,31 +799,41 @@ __global__ void __launch_bounds__(kFuseThreads, 1)
         for (int b = 0; b < MI; ++b)
 #pragma unroll
           for (int c = 0; c < 16; ++c) out[a][b][c] = 0.f;
+      // software pipeline over the unit's l_i^2 slots: the TMEM load of slot pt + 1 is in flight
+      // while slot pt is folded (two register buffers)
+      uint32_t rbuf[2][16];
+      const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * 16);
+      {
+        const uint32_t slot = sc % kSlots2, spar = (sc / kSlots2) & 1;
+        mbar_wait(smem_u32(&s_full[slot]), spar);
+        fence_after();
+        tmem_ld16(tq + slot * (uint32_t)kN2, rbuf[0]);
+      }
 #pragma unroll
-      for (int pih = 0; pih < LI; ++pih) {
-#pragma unroll
-        for (int piw = 0; piw < LI; ++piw, ++sc) {
-          const uint32_t slot = sc % kSlots2, spar = (sc / kSlots2) & 1;
-          mbar_wait(smem_u32(&s_full[slot]), spar);
+      for (int pt = 0; pt < LI * LI; ++pt, ++sc) {
+        const int pih = pt / LI, piw = pt % LI;
+        const uint32_t slot = sc % kSlots2;
+        tmem_ld_wait();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&s_empty[slot]));
+        if (pt + 1 < LI * LI) {
+          const uint32_t sn = (sc + 1) % kSlots2, spn = ((sc + 1) / kSlots2) & 1;
+          mbar_wait(smem_u32(&s_full[sn]), spn);
           fence_after();
-          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * (uint32_t)kN2 + (uint32_t)(half * 16);
-          uint32_t r0[16];
-          tmem_ld16(taddr, r0);
-          tmem_ld_wait();
-          fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&s_empty[slot]));
+          tmem_ld16(tq + sn * (uint32_t)kN2, rbuf[(pt + 1) & 1]);
+        }
 #pragma unroll
-          for (int jh = 0; jh < MI; ++jh) {
-            const float ah = float(rdouble(KI.AT[jh][pih]));
-            if (ah == 0.f) continue;
+        for (int jh = 0; jh < MI; ++jh) {
+          const float ah = float(rdouble(KI.AT[jh][pih]));
+          if (ah == 0.f) continue;
 #pragma unroll
-            for (int jw = 0; jw < MI; ++jw) {
-              const float a = ah * float(rdouble(KI.AT[jw][piw]));
-              if (a == 0.f) continue;
+          for (int jw = 0; jw < MI; ++jw) {
+            const float a = ah * float(rdouble(KI.AT[jw][piw]));
+            if (a == 0.f) continue;
 #pragma unroll
-              for (int c = 0; c < 16; ++c) out[jh][jw][c] = fmaf(a, __uint_as_float(r0[c]), out[jh][jw][c]);
-            }
+            for (int c = 0; c < 16; ++c)
+              out[jh][jw][c] = fmaf(a, __uint_as_float(rbuf[pt & 1][c]), out[jh][jw][c]);
           }
         }
       }
@@ -1007,9 +1026,9 @@ nw_status_t launch_gemm_tc_fused2(const nw_plan_st* p, const Geometry& g, const 
   prm.Mpp = Mpp;
   const uint32_t stage = (tc::kBM * prm.kbk * 2 + (uint32_t)tc::kN2 * prm.kbk * 2) * (prm.lo ? 2 : 1);
   prm.nst = (int)((200u * 1024u) / stage);
-  if (prm.nst > tc::kMaxStages) prm.nst = tc::kMaxStages;
+  if (prm.nst > tc::kMaxStages2) prm.nst = tc::kMaxStages2;
   if (prm.nst < 2) return NW_ERR_UNSUPPORTED;
-  size_t smem = 1024 + (size_t)stage * prm.nst + (2 * tc::kMaxStages + 2 * tc::kSlots2 + 2) * 8;
+  size_t smem = 1024 + (size_t)stage * prm.nst + (2 * tc::kMaxStages2 + 2 * tc::kSlots2 + 2) * 8;
   if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM: each CTA owns all 512 TMEM columns
   const long long rowsV = (long long)g.P * g.T_pad * (prm.lo ? 2 : 1);
   const long long rowsU = (long long)g.P * g.cout_pad * (prm.lo ? 2 : 1);
@@ -1036,7 +1055,7 @@ nw_status_t launch_gemm_tc_fused2(const nw_plan_st* p, const Geometry& g, const 
   if (CL > 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(tc::kFuseThreads);
+    cfg.blockDim = dim3(tc::kFuse2Threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -1048,7 +1067,7 @@ nw_status_t launch_gemm_tc_fused2(const nw_plan_st* p, const Geometry& g, const 
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, tc::contraction_fused2_kernel<3, 2>, mapV, mapU, prm) != cudaSuccess)
       return NW_ERR_CUDA;
-  } else if (launch_pdl(tc::contraction_fused2_kernel<3, 1>, dim3(grid), dim3(tc::kFuseThreads), smem, s, mapV, mapU,
+  } else if (launch_pdl(tc::contraction_fused2_kernel<3, 1>, dim3(grid), dim3(tc::kFuse2Threads), smem, s, mapV, mapU,
                         prm) != NW_OK) {
     return NW_ERR_CUDA;
   }
