@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* T_empty = bars + 4 * kMaxStages + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * kMaxStages + 4);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform (role branches and issue loops in uniform registers)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int total_units = p.P * p.ngrp;
   const int rank = (CL > 1) ? (int)cluster_rank() : 0;
   const int ustart = (CL > 1) ? (int)blockIdx.x / CL : (int)blockIdx.x;
@@ -244,8 +245,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   griddep_wait();  // V comes from the input transform just before in the stream
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------ TMA producer ------------------------------
+    {
+      // ------------------------------ TMA producer (warp-uniform loop, elected lane issues) ------------------------------
       int sa = 0, sb = 0;
       uint32_t pa = 0, pb = 0;
       for (int u = ustart; u < total_units; u += ustep) {
@@ -255,10 +256,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < p.KB; ++kb) {
           mbar_wait(smem_u32(&B_empty[sb]), pb ^ 1);
           const uint32_t bfull = smem_u32(&B_full[sb]);
-          mbar_expect_tx(bfull, b_stage);
           const uint32_t bdst = base + b_off + sb * b_stage;
           const int sh = kb / p.kbc, kc = kb - sh * p.kbc;
           const int bcol = sh * p.cin_pad + kc * p.kbk, acol = kc * p.kbk, aoff = p.shoff[sh];
+          if (elect_one()) {
+          mbar_expect_tx(bfull, b_stage);
           if constexpr (CL > 1) {
             const int rows = p.N / CL;  // this CTA's slice of the B tile, multicast to the cluster
             const uint32_t so = (uint32_t)(rank * rows) * (p.kbk * 2);
@@ -270,11 +272,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(bdst, &mapU, bfull, bcol, xi * p.N);
             if (p.lo) tma_load_2d(bdst + b_plane, &mapU, bfull, bcol, (int)(p.b_lo_row + (long long)xi * p.N));
           }
+          }
+          __syncwarp();
           if (++sb == p.nB) { sb = 0; pb ^= 1; }
           for (int g = 0; g < g_eff; ++g) {
             mbar_wait(smem_u32(&A_empty[sa]), pa ^ 1);
             const uint32_t afull = smem_u32(&A_full[sa]);
-            mbar_expect_tx(afull, a_stage);
             const uint32_t adst = base + a_off + sa * a_stage;
             long long row, lrow;
             if (p.vblk) {
@@ -284,17 +287,21 @@ __global__ void __launch_bounds__(kThreads, 1)
               row = (long long)xi * p.T_pad + (long long)(mb0 + g) * kBM + aoff;
               lrow = p.a_lo_row + row;
             }
-            tma_load_2d(adst, &mapV, afull, acol, (int)row);
-            if (p.lo) tma_load_2d(adst + a_plane, &mapV, afull, acol, (int)lrow);
+            if (elect_one()) {
+              mbar_expect_tx(afull, a_stage);
+              tma_load_2d(adst, &mapV, afull, acol, (int)row);
+              if (p.lo) tma_load_2d(adst + a_plane, &mapV, afull, acol, (int)lrow);
+            }
+            __syncwarp();
             if (++sa == p.nA) { sa = 0; pa ^= 1; }
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------- MMA issuer -------------------------------
-      const uint32_t idesc = idesc_bf16(p.N);
+    {
+      // ------------------------------- MMA issuer (warp-uniform loop, elected lane issues) -------------------------------
+      const uint32_t idesc = idesc_bf16(p.N), dhi = swk_desc_hi(p.kbk);
       int sa = 0, sb = 0;
       uint32_t pa = 0, pb = 0;
       int it = 0;
@@ -314,27 +321,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_after();
             const uint32_t asm_ = base + a_off + sa * a_stage;
             const uint32_t acc = acc0 + (uint32_t)(g * p.N);
-#pragma unroll
-            for (int k = 0; k < p.kbk / 16; ++k) {
-              const uint64_t ah = swk_desc(asm_ + k * 32, p.kbk);
-              const uint64_t bh = swk_desc(bsm + k * 32, p.kbk);
-              const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
-              umma_f16(acc, ah, bh, idesc, accum);
-              if (p.lo) {
-                const uint64_t al = swk_desc(asm_ + a_plane + k * 32, p.kbk);
-                const uint64_t bl = swk_desc(bsm + b_plane + k * 32, p.kbk);
-                umma_f16(acc, ah, bl, idesc, 1u);
-                umma_f16(acc, al, bh, idesc, 1u);
-              }
+            if (elect_one()) {
+              issue_kblock_any(p.kbk, acc, asm_ >> 4, bsm >> 4, a_plane >> 4, b_plane >> 4, dhi, idesc, p.lo,
+                               kb > 0 ? 1u : 0u);
+              umma_commit(smem_u32(&A_empty[sa]));
             }
-            umma_commit(smem_u32(&A_empty[sa]));
+            __syncwarp();
             if (++sa == p.nA) { sa = 0; pa ^= 1; }
           }
-          if constexpr (CL > 1) umma_commit_mc(smem_u32(&B_empty[sb]), kMask);  // frees the stage cluster-wide
-          else umma_commit(smem_u32(&B_empty[sb]));
+          if (elect_one()) {
+            if constexpr (CL > 1) umma_commit_mc(smem_u32(&B_empty[sb]), kMask);  // frees the stage cluster-wide
+            else umma_commit(smem_u32(&B_empty[sb]));
+          }
+          __syncwarp();
           if (++sb == p.nB) { sb = 0; pb ^= 1; }
         }
-        umma_commit(smem_u32(&T_full[buf]));
+        if (elect_one()) umma_commit(smem_u32(&T_full[buf]));
+        __syncwarp();
       }
     }
   } else {
