@@ -175,6 +175,8 @@ static nw_status_t forward_one(const nw_plan_st *p, const Geometry &g, const voi
     st = launch_gemm_simt(p, g, static_cast<const float *>(V), static_cast<const float *>(U), M, sg);
   else if (flevel == 2)
     st = launch_gemm_tc_fused2(p, g, V, U, M, sg);
+  else if (fused && gemm_fused_wide(p, g))
+    st = launch_gemm_tc_fused1c(p, g, V, U, M, sg);
   else if (fused)
     st = launch_gemm_tc_fused(p, g, V, U, M, sg);
   else

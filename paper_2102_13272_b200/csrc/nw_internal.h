@@ -117,6 +117,10 @@ nw_status_t launch_gemm_tc_fused(const nw_plan_st *p, const Geometry &g, const v
 // fusion level of the contraction epilogue: 0 plain (M), 1 inner output level along w (M'),
 // 2 inner level along both axes (M'' = (m_i / l_i)^2 of M)
 int gemm_fused_level(const nw_plan_st *p, const Geometry &g);
+// wide layers (Cout_pad 128 / 256): level 1 with 128-channel CTAs (pairs multicast the A tiles)
+bool gemm_fused_wide(const nw_plan_st *p, const Geometry &g);
+nw_status_t launch_gemm_tc_fused1c(const nw_plan_st *p, const Geometry &g, const void *V, const void *U, float *Mp,
+                                   cudaStream_t s);
 nw_status_t launch_gemm_tc_fused2(const nw_plan_st *p, const Geometry &g, const void *V, const void *U, float *Mpp,
                                   cudaStream_t s);
 nw_status_t launch_output_transform_pre2(const nw_plan_st *p, const Geometry &g, const float *Mpp, void *y,

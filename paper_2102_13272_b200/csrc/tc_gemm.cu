@@ -868,6 +868,195 @@ __global__ void __launch_bounds__(kFuse2Threads, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tcols));
 }
 
+// ---------------------------------------------------------------------------
+// Level-1 fusion for wide layers (Cout_pad = 128 or 256, e.g. C3): the inner output level along
+// w in the epilogue, 128 channels per CTA.  Five 256-column accumulators do not fit TMEM and a
+// 64-channel unit would re-read every A tile four times, so the two 128-channel halves of a
+// (point group, block) run on the two CTAs of a cluster that multicast the A tiles to each other
+// (same scheme as contraction_fused2_kernel).  4 TMEM slots of 128 columns; 8 epilogue warps
+// (lane quarter x 64 columns) hold m_i x 64 partial sums each (setmaxnreg 232).  M' is 3/5 of M.
+// ---------------------------------------------------------------------------
+constexpr int kSlotsC = 4;
+constexpr int kNC = 128;
+
+template <int MI, int CL>
+__global__ void __launch_bounds__(kFuse2Threads, 1)
+    contraction_fused1c_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapU,
+                               const Fused2Params p) {
+  constexpr int LI = MI + 2;
+  constexpr Kernel1D KI = make_kernel(MI, 3);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* sbase = smem_raw + (base - raw);
+  const uint32_t a_plane = kBM * p.kbk * 2, b_plane = (uint32_t)kNC * p.kbk * 2;
+  const uint32_t a_bytes = a_plane * (p.lo ? 2 : 1), b_bytes = b_plane * (p.lo ? 2 : 1);
+  const uint32_t stage = a_bytes + b_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + (size_t)stage * p.nst);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kMaxStages2;
+  uint64_t* s_full = bars + 2 * kMaxStages2;
+  uint64_t* s_empty = bars + 2 * kMaxStages2 + kSlotsC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages2 + 2 * kSlotsC);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int units = p.nmb * p.PA * p.LO;  // (point group, block) per CTA (CL = 1) or per pair
+  const int rank = (CL > 1) ? (int)cluster_rank() : 0;
+  const int ustart = (int)blockIdx.x / CL, ustep = (int)gridDim.x / CL;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
+  constexpr uint32_t tcols = kSlotsC * kNC;  // 512
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapV);
+    tma_prefetch(&mapU);
+    for (int i = 0; i < p.nst; ++i) { mbar_init(smem_u32(&full[i]), 1); mbar_init(smem_u32(&empty[i]), CL); }
+    for (int i = 0; i < kSlotsC; ++i) { mbar_init(smem_u32(&s_full[i]), 1); mbar_init(smem_u32(&s_empty[i]), 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(tcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+  }
+  fence_before();
+  __syncthreads();
+  if constexpr (CL > 1) cluster_sync();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_launch_dependents();
+  griddep_wait();
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if (warp == 0) {  // ------------------------- TMA producer -------------------------
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = ustart; u < units; u += ustep) {
+        const int pg = u / p.nmb, mb = u - pg * p.nmb;
+        const int p_h = pg / p.LO, p_o = pg - p_h * p.LO;
+        for (int pi = 0; pi < LI; ++pi) {
+          const int xi = p_h * p.PA + p_o * LI + pi;
+          for (int kb = 0; kb < p.KB; ++kb) {
+            mbar_wait(smem_u32(&empty[st]), ph ^ 1);
+            const uint32_t fb = smem_u32(&full[st]);
+            const uint32_t dst = base + (uint32_t)st * stage;
+            long long row, lrow;
+            if (p.vblk) {
+              row = ((long long)mb * p.P + xi) * (2 * kBM);
+              lrow = row + kBM;
+            } else {
+              row = (long long)xi * p.T_pad + (long long)mb * kBM;
+              lrow = p.a_lo_row + row;
+            }
+            if (elect_one()) {
+              mbar_expect_tx(fb, stage);
+              if constexpr (CL > 1) {
+                const int hr = kBM / CL;
+                const uint32_t so = (uint32_t)(rank * hr) * (uint32_t)(p.kbk * 2);
+                tma_load_2d_mc(dst + so, &mapV, fb, kb * p.kbk, (int)row + rank * hr, kMask);
+                if (p.lo) tma_load_2d_mc(dst + a_plane + so, &mapV, fb, kb * p.kbk, (int)lrow + rank * hr, kMask);
+              } else {
+                tma_load_2d(dst, &mapV, fb, kb * p.kbk, (int)row);
+                if (p.lo) tma_load_2d(dst + a_plane, &mapV, fb, kb * p.kbk, (int)lrow);
+              }
+              const int brow = xi * p.N + rank * kNC;
+              tma_load_2d(dst + a_bytes, &mapU, fb, kb * p.kbk, brow);
+              if (p.lo) tma_load_2d(dst + a_bytes + b_plane, &mapU, fb, kb * p.kbk, (int)(p.b_lo_row + brow));
+            }
+            __syncwarp();
+            if (++st == p.nst) { st = 0; ph ^= 1; }
+          }
+        }
+      }
+    } else if (warp == 1) {  // ------------------------- MMA issuer ---------------------------
+      const uint32_t idesc = idesc_bf16(kNC), dhi = swk_desc_hi(p.kbk);
+      int st = 0;
+      uint32_t ph = 0;
+      uint32_t sc = 0;
+      for (int u = ustart; u < units; u += ustep) {
+        for (int pi = 0; pi < LI; ++pi, ++sc) {
+          const uint32_t slot = sc % kSlotsC, spar = (sc / kSlotsC) & 1;
+          mbar_wait(smem_u32(&s_empty[slot]), spar ^ 1);
+          fence_after();
+          const uint32_t acc = tmem_base + slot * (uint32_t)kNC;
+          for (int kb = 0; kb < p.KB; ++kb) {
+            mbar_wait(smem_u32(&full[st]), ph);
+            fence_after();
+            const uint32_t asm_ = base + (uint32_t)st * stage, bsm = asm_ + a_bytes;
+            if (elect_one()) {
+              issue_kblock_any(p.kbk, acc, asm_ >> 4, bsm >> 4, a_plane >> 4, b_plane >> 4, dhi, idesc, p.lo,
+                               kb > 0 ? 1u : 0u);
+              if constexpr (CL > 1) umma_commit_mc(smem_u32(&empty[st]), kMask);
+              else umma_commit(smem_u32(&empty[st]));
+            }
+            __syncwarp();
+            if (++st == p.nst) { st = 0; ph ^= 1; }
+          }
+          if (elect_one()) umma_commit(smem_u32(&s_full[slot]));
+          __syncwarp();
+        }
+      }
+    }
+  } else {  // ------------------------------- epilogue (warpgroups 1 and 2) ----------------------------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+    const int q = warp & 3, half = (warp - 4) >> 2;
+    uint32_t sc = 0;
+    for (int u = ustart; u < units; u += ustep) {
+      const int pg = u / p.nmb, mb = u - pg * p.nmb;
+      float out[MI][64];
+#pragma unroll
+      for (int s2 = 0; s2 < MI; ++s2)
+#pragma unroll
+        for (int c = 0; c < 64; ++c) out[s2][c] = 0.f;
+#pragma unroll
+      for (int pi = 0; pi < LI; ++pi, ++sc) {
+        const uint32_t slot = sc % kSlotsC, spar = (sc / kSlotsC) & 1;
+        mbar_wait(smem_u32(&s_full[slot]), spar);
+        fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + slot * (uint32_t)kNC + (uint32_t)(half * 64);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t r0[16];
+          tmem_ld16(taddr + ch * 16, r0);
+          tmem_ld_wait();
+          if (ch == 3) {  // the slot's last columns are in registers: release it
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&s_empty[slot]));
+          }
+#pragma unroll
+          for (int s2 = 0; s2 < MI; ++s2) {
+            const float a = float(rdouble(KI.AT[s2][pi]));
+            if (a == 0.f) continue;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) out[s2][ch * 16 + c] = fmaf(a, __uint_as_float(r0[c]), out[s2][ch * 16 + c]);
+          }
+        }
+      }
+      {
+        const long long t = (long long)mb * kBM + q * 32 + lane;
+        const int col0 = rank * kNC + half * 64;
+        const long long pitch = p.T_pad;
+#pragma unroll
+        for (int s2 = 0; s2 < MI; ++s2) {
+          float* dst = p.Mpp + ((long long)(pg * MI + s2) * p.N + col0) * p.T_pad + t;
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            *dst = out[s2][c];
+            long long w = pitch;
+            asm volatile("" : "+l"(w));
+            dst += w;
+          }
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if constexpr (CL > 1) cluster_sync();
+  fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tcols));
+}
+
 }  // namespace tc
 
 // ------------------------------ host side ------------------------------------
@@ -1004,9 +1193,84 @@ bool gemm_fused_eligible(const nw_plan_st* p, const Geometry& g) {
 }
 // 0: plain contraction (M), 1: M' (inner level along w), 2: M'' (inner level along both axes;
 // stream-ordered launches only: the streamed pipeline's counters belong to level 1)
+// wide layers (Cout_pad 128 / 256): level 1 on 128-channel CTAs / CTA pairs (contraction_fused1c_kernel);
+// NW_FUSE_WIDE=0 keeps the plain contraction
+bool gemm_fused_wide(const nw_plan_st* p, const Geometry& g) {
+  static const int on = [] {
+    const char* v = getenv("NW_FUSE_WIDE");
+    return v ? atoi(v) : 1;
+  }();
+  return on && fuse_ai_env() && !p->depthwise && g.path == kPathNested && p->math != NW_MATH_FP32_SIMT &&
+         (g.cout_pad == 128 || g.cout_pad == 256) && g.mi == 3 && g.nsh == 1 && !g.sync && !g.sync2 &&
+         (g.gemm_ctas <= 0 || g.gemm_ctas >= 2);
+}
 int gemm_fused_level(const nw_plan_st* p, const Geometry& g) {
+  if (gemm_fused_wide(p, g)) return 1;
   if (!gemm_fused_eligible(p, g)) return 0;
   return (fuse_ai_env() >= 2 && !g.sync && !g.sync2) ? 2 : 1;
+}
+
+nw_status_t launch_gemm_tc_fused1c(const nw_plan_st* p, const Geometry& g, const void* V, const void* U, float* Mp,
+                                   cudaStream_t s) {
+  tc::Fused2Params prm{};
+  prm.nmb = (int)(g.T_pad / tc::kBM);
+  prm.N = g.cout_pad;
+  prm.nhalf = g.cout_pad / tc::kNC;
+  prm.kbk = pick_kbk(g.cin_pad);
+  prm.KB = (g.cin_pad + prm.kbk - 1) / prm.kbk;
+  prm.lo = (p->math == NW_MATH_BF16X3) ? 1 : 0;
+  const NestedAxis ax = path_axis(p, g.path);
+  prm.PA = ax.Pa;
+  prm.LO = ax.l_o;
+  prm.T_pad = g.T_pad;
+  prm.a_lo_row = (long long)g.P * g.T_pad;
+  prm.b_lo_row = (long long)g.P * g.cout_pad;
+  prm.P = g.P;
+  prm.vblk = (g.vblk && prm.lo) ? 1 : 0;
+  prm.Mpp = Mp;
+  const uint32_t stage = (tc::kBM * prm.kbk * 2 + (uint32_t)tc::kNC * prm.kbk * 2) * (prm.lo ? 2 : 1);
+  prm.nst = (int)((200u * 1024u) / stage);
+  if (prm.nst > tc::kMaxStages2) prm.nst = tc::kMaxStages2;
+  if (prm.nst < 2) return NW_ERR_UNSUPPORTED;
+  size_t smem = 1024 + (size_t)stage * prm.nst + (2 * tc::kMaxStages2 + 2 * tc::kSlotsC + 2) * 8;
+  if (smem < 120 * 1024) smem = 120 * 1024;  // one CTA per SM: each CTA owns all 512 TMEM columns
+  const long long rowsV = (long long)g.P * g.T_pad * (prm.lo ? 2 : 1);
+  const long long rowsU = (long long)g.P * g.cout_pad * (prm.lo ? 2 : 1);
+  if (rowsV >= (1ll << 31)) return NW_ERR_UNSUPPORTED;
+  alignas(64) CUtensorMap mapV, mapU;
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (g.gemm_ctas > 0 && g.gemm_ctas < sms) sms = g.gemm_ctas;
+  const int CL = prm.nhalf;  // 1 or 2
+  if (!make_map(&mapV, V, rowsV, g.cin_pad, tc::kBM / CL, prm.kbk)) return NW_ERR_CUDA;
+  if (!make_map(&mapU, U, rowsU, g.cin_pad, tc::kNC, prm.kbk)) return NW_ERR_CUDA;
+  if ((CL > 1 ? ensure_smem<tc::contraction_fused1c_kernel<3, 2>>(227 * 1024)
+              : ensure_smem<tc::contraction_fused1c_kernel<3, 1>>(227 * 1024)) != NW_OK)
+    return NW_ERR_CUDA;
+  const long long units = (long long)prm.nmb * prm.PA * prm.LO * CL;  // CTA-units
+  int grid = (int)(units < sms ? units : sms);
+  if (grid > CL) grid -= grid % CL;
+  LaunchScope scope_("contraction_tc", s);
+  if (CL > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tc::kFuse2Threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, tc::contraction_fused1c_kernel<3, 2>, mapV, mapU, prm) != cudaSuccess)
+      return NW_ERR_CUDA;
+  } else if (launch_pdl(tc::contraction_fused1c_kernel<3, 1>, dim3(grid), dim3(tc::kFuse2Threads), smem, s, mapV,
+                        mapU, prm) != NW_OK) {
+    return NW_ERR_CUDA;
+  }
+  return check_launch();
 }
 
 nw_status_t launch_gemm_tc_fused2(const nw_plan_st* p, const Geometry& g, const void* V, const void* U, float* Mpp,
