@@ -31,7 +31,9 @@
  *  - Environment tunables (performance only; results are bit-identical or within
  *    rounding order, never a different algorithm): NW_FUSE_AI=0 disables the
  *    inner output level in the contraction epilogue, 1 applies it along w only (default 2:
- *    along both axes); NW_IN_CC=16|32|64 source
+ *    along both axes); NW_FUSE_WIDE=0 keeps the plain contraction for layers with 128 / 256
+ *    padded output channels (default: inner level along w on 128-channel CTAs / CTA pairs),
+ *    NW_KBK_WIDE=16|32 narrows that kernel's K block (measured slower); NW_IN_CC=16|32|64 source
  *    channels per input-transform CTA (default 32); NW_PIPE_CHUNKS=k runs
  *    nw_conv_forward as a k-chunk three-stream pipeline (default 1) and
  *    NW_GEMM_CTAS caps its contraction grid; NW_HOST_CHUNKS=k sets the chunk

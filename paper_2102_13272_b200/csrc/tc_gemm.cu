@@ -1216,7 +1216,14 @@ nw_status_t launch_gemm_tc_fused1c(const nw_plan_st* p, const Geometry& g, const
   prm.nmb = (int)(g.T_pad / tc::kBM);
   prm.N = g.cout_pad;
   prm.nhalf = g.cout_pad / tc::kNC;
+  // K block width: 64 KB stages (kbk 64) leave two stages of loads in flight behind the one being
+  // multiplied; narrower blocks keep more bytes in flight in the same shared memory (NW_KBK_WIDE)
+  static const int kbk_env = [] {
+    const char* v = getenv("NW_KBK_WIDE");
+    return v ? atoi(v) : 0;
+  }();
   prm.kbk = pick_kbk(g.cin_pad);
+  if ((kbk_env == 16 || kbk_env == 32) && g.cin_pad % kbk_env == 0 && prm.kbk > kbk_env) prm.kbk = kbk_env;
   prm.KB = (g.cin_pad + prm.kbk - 1) / prm.kbk;
   prm.lo = (p->math == NW_MATH_BF16X3) ? 1 : 0;
   const NestedAxis ax = path_axis(p, g.path);

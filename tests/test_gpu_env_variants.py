@@ -87,6 +87,10 @@ BITWISE = [
 def test_scheduling_tunables_bit_identical(spec, env, tmp_path):
     # the streamed pipeline's counters belong to the w-only fused contraction (NW_FUSE_AI=1)
     base = {"NW_FUSE_AI": "1"} if "NW_STREAM" in env else None
+    # C3's scheduling tunables belong to the plain contraction (the default for 256 output channels
+    # is the 128-channel fused kernel, NW_FUSE_WIDE)
+    if spec.get("config") == "c3" and spec.get("Cout") == 256:
+        base = {"NW_FUSE_WIDE": "0"}
     y0 = _run(dict(spec), base, tmp=tmp_path)
     y1 = _run(dict(spec), {**env, **(base or {})}, tmp=tmp_path)
     assert y0.shape == y1.shape
@@ -97,11 +101,13 @@ ARITH = [
     (C2, {"NW_FUSE_AI": "0"}),
     (C2, {"NW_FUSE_AI": "1"}),      # inner output level along w only (default 2: both axes)
     (C4B, {"NW_FUSE_AI": "1"}),
+    (C3, {"NW_FUSE_WIDE": "0"}),    # plain contraction instead of the 128-channel fused kernel
+    ({**C3, "Cout": 128}, {"NW_FUSE_AI": "2"}),   # 128 output channels: the fused kernel without a CTA pair
     ({"config": "c5_conv1", "N": 2, "H": 37, "W": 45}, {"NW_FUSED_C1": "0"}),
 ]
 
 
-@pytest.mark.parametrize("spec,env", ARITH, ids=["fuse_ai_off", "fuse_ai_w_c2", "fuse_ai_w_c4b", "fused_c1_off"])
+@pytest.mark.parametrize("spec,env", ARITH, ids=["fuse_ai_off", "fuse_ai_w_c2", "fuse_ai_w_c4b", "fuse_wide_off", "fuse_wide_128", "fused_c1_off"])
 def test_arithmetic_tunables_meet_gate(spec, env, tmp_path):
     y = _run(dict(spec), env, tmp=tmp_path)
     s = dict(spec)
