@@ -803,7 +803,25 @@ __global__ void __launch_bounds__(kFuse2Threads, 1)
 #pragma unroll
           for (int c = 0; c < 16; ++c) out[a][b][c] = 0.f;
       // software pipeline over the unit's l_i^2 slots: the TMEM load of slot pt + 1 is in flight
-      // while slot pt is folded (two register buffers)
+      // while slot pt is folded (two register buffers).  A partial sum (j_h, j_w) is final after the
+      // last point with non-zero A_i^T[j_h][p_ih] A_i^T[j_w][p_iw]; it is stored right then, so most
+      // of the unit's 144 stores per thread overlap the remaining points instead of queueing up in
+      // the load/store unit after the last one.
+      const long long t = (long long)mb * kBM + q * 32 + lane;
+      const int col0 = nh * kN2 + half * 16;
+      const int rl = p.LO * MI;  // M'' values per row of the (p_oh, j_h) grid
+      const long long pitch = p.T_pad;
+      auto store_out = [&](int jh, int jw) {
+        const long long R = (long long)(p_oh * MI + jh) * rl + p_ow * MI + jw;
+        float* dst = p.Mpp + (R * p.N + col0) * p.T_pad + t;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          *dst = out[jh][jw][c];
+          long long w = pitch;
+          asm volatile("" : "+l"(w));  // keep the walk incremental (no hoisted per-store offsets)
+          dst += w;
+        }
+      };
       uint32_t rbuf[2][16];
       const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * 16);
       {
@@ -839,23 +857,18 @@ __global__ void __launch_bounds__(kFuse2Threads, 1)
               out[jh][jw][c] = fmaf(a, __uint_as_float(rbuf[pt & 1][c]), out[jh][jw][c]);
           }
         }
-      }
-      const long long t = (long long)mb * kBM + q * 32 + lane;
-      const int col0 = nh * kN2 + half * 16;
-      const int rl = p.LO * MI;  // M'' values per row of the (p_oh, j_h) grid
-      const long long pitch = p.T_pad;
+        // partial sums whose last contributing point this was
 #pragma unroll
-      for (int jh = 0; jh < MI; ++jh) {
+        for (int jh = 0; jh < MI; ++jh) {
 #pragma unroll
-        for (int jw = 0; jw < MI; ++jw) {
-          const long long R = (long long)(p_oh * MI + jh) * rl + p_ow * MI + jw;
-          float* dst = p.Mpp + (R * p.N + col0) * p.T_pad + t;
+          for (int jw = 0; jw < MI; ++jw) {
+            int lh = 0, lw = 0;
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            *dst = out[jh][jw][c];
-            long long w = pitch;
-            asm volatile("" : "+l"(w));  // keep the walk incremental (no hoisted per-store offsets)
-            dst += w;
+            for (int k = 0; k < LI; ++k) {
+              if (rdouble(KI.AT[jh][k]) != 0.0) lh = k;
+              if (rdouble(KI.AT[jw][k]) != 0.0) lw = k;
+            }
+            if (pih == lh && piw == lw) store_out(jh, jw);
           }
         }
       }
