@@ -1020,6 +1020,21 @@ __global__ void __launch_bounds__(kFuse2Threads, 1)
       for (int s2 = 0; s2 < MI; ++s2)
 #pragma unroll
         for (int c = 0; c < 64; ++c) out[s2][c] = 0.f;
+      const long long t = (long long)mb * kBM + q * 32 + lane;
+      const int col0 = rank * kNC + half * 64;
+      const long long pitch = p.T_pad;
+      // a partial sum is stored as soon as its last contributing point is folded (two of the three
+      // rows after point l_i - 2), so most stores overlap the unit's last point
+      auto store_out = [&](int s2) {
+        float* dst = p.Mpp + ((long long)(pg * MI + s2) * p.N + col0) * p.T_pad + t;
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          *dst = out[s2][c];
+          long long w = pitch;
+          asm volatile("" : "+l"(w));
+          dst += w;
+        }
+      };
 #pragma unroll
       for (int pi = 0; pi < LI; ++pi, ++sc) {
         const uint32_t slot = sc % kSlotsC, spar = (sc / kSlotsC) & 1;
@@ -1044,21 +1059,13 @@ __global__ void __launch_bounds__(kFuse2Threads, 1)
             for (int c = 0; c < 16; ++c) out[s2][ch * 16 + c] = fmaf(a, __uint_as_float(r0[c]), out[s2][ch * 16 + c]);
           }
         }
-      }
-      {
-        const long long t = (long long)mb * kBM + q * 32 + lane;
-        const int col0 = rank * kNC + half * 64;
-        const long long pitch = p.T_pad;
 #pragma unroll
         for (int s2 = 0; s2 < MI; ++s2) {
-          float* dst = p.Mpp + ((long long)(pg * MI + s2) * p.N + col0) * p.T_pad + t;
+          int last = 0;
 #pragma unroll
-          for (int c = 0; c < 64; ++c) {
-            *dst = out[s2][c];
-            long long w = pitch;
-            asm volatile("" : "+l"(w));
-            dst += w;
-          }
+          for (int k = 0; k < LI; ++k)
+            if (rdouble(KI.AT[s2][k]) != 0.0) last = k;
+          if (pi == last) store_out(s2);
         }
       }
     }
