@@ -12,13 +12,14 @@ def _info(l):
 
 
 def test_c2k9_bytes_match_design_table():
-    # per slice V = 900 points x 4 B per channel, M' = 540 rows x 4 B
+    # per slice V = 900 points x 4 B per channel, M'' = (l_o m_i)^2 = 324 rows x 4 B
+    # (the contraction's epilogue applies the inner output level along both axes)
     l = synth.CONFIGS["c2k9"]
     w = bench.kernel_work(l, _info(l), "bf16x3")
     T = l.N * 11 * 11                          # 128 / 12 -> 11 tiles per axis
     x_b = l.N * l.Cin * l.H * l.W * 4
     assert w["input_transform"]["bytes"] == x_b + 900 * T * 64 * 4
-    assert w["contraction_tc"]["bytes"] == 900 * T * 64 * 4 + 900 * 64 * 64 * 4 + 540 * T * 64 * 4
+    assert w["contraction_tc"]["bytes"] == 900 * T * 64 * 4 + 900 * 64 * 64 * 4 + 324 * T * 64 * 4
     assert w["contraction_tc"]["flops"] == 3 * 2 * 900 * T * 64 * 64
 
 
