@@ -49,6 +49,9 @@ BITWISE = [
     (C2, {"NW_IN_CC": "16"}),
     (C2, {"NW_IN_CC": "64"}),
     (C3, {"NW_CLUSTER": "1"}),
+    (C2, {"NW_CLUSTER": "1"}),                # level-2 fused contraction without CTA pairs (no A multicast)
+    (C4B, {"NW_CLUSTER": "1"}),
+    ({**C2, "N": 7, "H": 50, "W": 45}, {"NW_PIPE_CHUNKS": "2", "NW_GEMM_CTAS": "3"}),   # odd grid cap: pairs + a spare CTA slot
     (C3, {"NW_GEMM_G": "1"}),
     (C3, {"NW_PDL": "1"}),
     (C4B, {"NW_KBK": "64"}),
