@@ -680,6 +680,11 @@ __global__ void __launch_bounds__(kFuse2Threads, 1)
   const int ustart = (int)blockIdx.x / CL, ustep = (int)gridDim.x / CL;
   constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
   constexpr uint32_t tcols = kSlots2 * kN2;  // 512
+  // 3 groups of l_i slots are in use: the epilogue releases a whole group at once (one
+  // tcgen05 fence + arrive per l_i points instead of per point: the per-point release was a
+  // third of the epilogue's time on small-K layers), the MMA warp waits once per group
+  constexpr uint32_t kUsed = 3 * LI;
+  static_assert(kUsed <= kSlots2, "slot groups");
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mapV);
@@ -764,9 +769,11 @@ __global__ void __launch_bounds__(kFuse2Threads, 1)
       uint32_t sc = 0;
       for (int u = ustart; u < units; u += ustep) {
         for (int pt = 0; pt < LI * LI; ++pt, ++sc) {
-          const uint32_t slot = sc % kSlots2, spar = (sc / kSlots2) & 1;
-          mbar_wait(smem_u32(&s_empty[slot]), spar ^ 1);
-          fence_after();
+          const uint32_t slot = sc % kUsed, spar = (sc / kUsed) & 1;
+          if (slot % LI == 0) {  // first slot of a group: the epilogue has drained the group's previous use
+            mbar_wait(smem_u32(&s_empty[slot / LI]), spar ^ 1);
+            fence_after();
+          }
           const uint32_t acc = tmem_base + slot * (uint32_t)kN2;
           for (int kb = 0; kb < p.KB; ++kb) {
             mbar_wait(smem_u32(&full[st]), ph);
@@ -825,7 +832,7 @@ __global__ void __launch_bounds__(kFuse2Threads, 1)
       uint32_t rbuf[2][16];
       const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * 16);
       {
-        const uint32_t slot = sc % kSlots2, spar = (sc / kSlots2) & 1;
+        const uint32_t slot = sc % kUsed, spar = (sc / kUsed) & 1;
         mbar_wait(smem_u32(&s_full[slot]), spar);
         fence_after();
         tmem_ld16(tq + slot * (uint32_t)kN2, rbuf[0]);
@@ -833,13 +840,15 @@ __global__ void __launch_bounds__(kFuse2Threads, 1)
 #pragma unroll
       for (int pt = 0; pt < LI * LI; ++pt, ++sc) {
         const int pih = pt / LI, piw = pt % LI;
-        const uint32_t slot = sc % kSlots2;
+        const uint32_t slot = sc % kUsed;
         tmem_ld_wait();
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&s_empty[slot]));
+        if (pt % LI == LI - 1) {  // the group's last slot is in registers: release the group
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&s_empty[slot / LI]));
+        }
         if (pt + 1 < LI * LI) {
-          const uint32_t sn = (sc + 1) % kSlots2, spn = ((sc + 1) / kSlots2) & 1;
+          const uint32_t sn = (sc + 1) % kUsed, spn = ((sc + 1) / kUsed) & 1;
           mbar_wait(smem_u32(&s_full[sn]), spn);
           fence_after();
           tmem_ld16(tq + sn * (uint32_t)kN2, rbuf[(pt + 1) & 1]);
